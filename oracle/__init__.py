@@ -1,0 +1,117 @@
+"""CPU oracle for the DG S_N sweep + gray SM closures (ctypes over sweep_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product package
+paper_2504_21784_b200.  See sweep_oracle.c for what is computed and the
+PAPER.md passages each step follows.
+
+Parity status: pinned (tests/test_oracle_pins.py) — dense global assembly in
+the paper's jump/average form, closed-form 1-D transmission, constant-solution
+exactness, global particle balance, convergence order, rotation symmetry,
+quadrature identities.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sweep_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile sweep_oracle.c -> liboracle.so (gcc, -O2, OpenMP, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        i, d = ctypes.c_int, ctypes.c_double
+        lib.oracle_sweep.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, dp, i]
+        lib.oracle_sweep.restype = i
+        lib.oracle_sweep_psi.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, i, i, dp]
+        lib.oracle_sweep_psi.restype = i
+        lib.oracle_alpha.argtypes = [i, i, dp, dp, dp]
+        lib.oracle_alpha.restype = None
+        lib.oracle_out_size.argtypes = [i, i, i, i]
+        lib.oracle_out_size.restype = i
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _c(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def out_size(dim: int, nx: int, ny: int, p: int) -> int:
+    return _load().oracle_out_size(dim, nx, ny if dim == 2 else 1, p)
+
+
+def sweep(prob, nthreads: int = 0) -> np.ndarray:
+    """Packed gray output phi|J|T|beta|J+ (same layout as closures_get)."""
+    lib = _load()
+    om, w, s, q, fl = _c(prob.omega), _c(prob.w), _c(prob.sigma), _c(prob.q), _c(prob.inflow)
+    out = np.zeros(out_size(prob.dim, prob.nx, prob.ny, prob.p))
+    rc = lib.oracle_sweep(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
+                          s.shape[1], _ptr(s), float(prob.inv_c_dt), _ptr(q), _ptr(fl), _ptr(out), int(nthreads))
+    if rc != 0:
+        raise RuntimeError(f"oracle_sweep failed rc={rc}")
+    return out
+
+
+def sweep_psi(prob, d: int, g: int) -> np.ndarray:
+    """psi_{d,g} as [N_el][n]."""
+    lib = _load()
+    om, w, s, q, fl = _c(prob.omega), _c(prob.w), _c(prob.sigma), _c(prob.q), _c(prob.inflow)
+    n = (prob.p + 1) ** prob.dim
+    psi = np.zeros((prob.nx * (prob.ny if prob.dim == 2 else 1), n))
+    rc = lib.oracle_sweep_psi(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
+                              s.shape[1], _ptr(s), float(prob.inv_c_dt), _ptr(q), _ptr(fl), d, g, _ptr(psi))
+    if rc != 0:
+        raise RuntimeError(f"oracle_sweep_psi failed rc={rc}")
+    return psi
+
+
+def alpha(prob) -> np.ndarray:
+    """alpha for outward normals x-, x+, y-, y+ (eq:alpha)."""
+    lib = _load()
+    om, w = _c(prob.omega), _c(prob.w)
+    a = np.zeros(4)
+    lib.oracle_alpha(prob.dim, om.shape[0], _ptr(om), _ptr(w), _ptr(a))
+    return a
+
+
+def unpack(out: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
+    """Split a packed output into named fields (oracle side's own layout reader)."""
+    n = (p + 1) ** dim
+    nel = nx * (ny if dim == 2 else 1)
+    nodes = nel * n
+    nb = 2 if dim == 1 else 2 * (nx + ny) * (p + 1)
+    o = 0
+    f = {}
+    f["phi"] = out[o:o + nodes].reshape(nel, n); o += nodes
+    f["J"] = out[o:o + dim * nodes].reshape(dim, nel, n); o += dim * nodes
+    nT = 1 if dim == 1 else 3
+    f["T"] = out[o:o + nT * nodes].reshape(nT, nel, n); o += nT * nodes
+    f["beta"] = out[o:o + nb]; o += nb
+    f["Jplus"] = out[o:o + nb]; o += nb
+    assert o == out.size
+    return f

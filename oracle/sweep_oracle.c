@@ -1,0 +1,420 @@
+/*
+ * sweep_oracle.c — CPU ORACLE for the DG S_N sweep + gray SM closures.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with the CUDA path
+ * (paper_2504_21784_b200/csrc), and the CUDA path never calls it.
+ *
+ * What it computes (PAPER.md, arXiv 2504.21784):
+ *   For every direction d and group g, psi_{d,g} in Y_p solving the lumped
+ *   upwind-DG weak form of
+ *       Omega_d . grad psi + sigma~_g psi = q_g,   sigma~ = sigma_t + 1/(c dt)
+ *   (eq:smm_be_transport PAPER.md:219, sigma~ PAPER.md:239; weak form
+ *   eq:dgsn_transport PAPER.md:332-336 with the upwind flux PAPER.md:299-327;
+ *   every integral evaluated with the tensor Gauss-Lobatto rule).
+ *   Each high-order solve "inverts the left hand side only":
+ *   q is a given nodal source.  Then the gray sums over d and g
+ *       phi = sum w psi              (c E,  PAPER.md:156-158)
+ *       J   = sum w Omega psi        (F,    PAPER.md:160-161)
+ *       T   = sum w (Omega Omega - I/3) psi
+ *       beta = sum w (|Omega.n| - alpha) psi  on boundary face nodes
+ *       alpha = sum w |Omega.n| / sum w       (eq:alpha PAPER.md:173-175)
+ *       J+  = sum_{Omega.n>0} w (Omega.n) psi on boundary face nodes
+ *
+ * How (deliberately plain): for each (d,g), elements are visited in upwind
+ * nested-loop order; the element matrix is assembled UNSCALED straight from
+ * the weak form and solved with partial-pivot LU; contributions are summed
+ * with Neumaier compensation.  No closed forms, no Kronecker structure.
+ *
+ * Readings of the paper: R1 GLL nodal basis of order p with the
+ * collocated (p+1)-point GLL rule for p = 2; R2 nodal source; R3 sum w = 1, no
+ * 1/(4 pi); R4 T components xx (1-D) or xx,xy,yy (2-D); R5 beta/J+ from the
+ * element's own nodal trace for every direction; R6 alpha per normal;
+ * R15 Omega.n = 0 gives no face term.
+ *
+ * Parity pins: tests/test_oracle_pins.py (dense global assembly in the
+ * jump/average form, closed-form 1-D transmission, constant-solution
+ * exactness, particle balance, convergence order, symmetries).
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define MAXN 9   /* (p+1)^dim <= 9 */
+
+/* ---- reference element: GLL nodes/weights on [0,1] and D_ab = l_b'(xi_a) ---- */
+typedef struct {
+    int p, np1;
+    double xi[3], wh[3];
+    double D[3][3];
+} refel;
+
+static int make_refel(int p, refel *R) {
+    if (p == 1) {
+        R->xi[0] = 0.0; R->xi[1] = 1.0;
+        R->wh[0] = 0.5; R->wh[1] = 0.5;
+    } else if (p == 2) {
+        R->xi[0] = 0.0; R->xi[1] = 0.5; R->xi[2] = 1.0;
+        R->wh[0] = 1.0 / 6.0; R->wh[1] = 2.0 / 3.0; R->wh[2] = 1.0 / 6.0;
+    } else {
+        return -1;
+    }
+    R->p = p; R->np1 = p + 1;
+    /* derivative of the Lagrange basis l_b at node xi_a, from its definition */
+    for (int a = 0; a <= p; ++a)
+        for (int b = 0; b <= p; ++b) {
+            double s = 0.0;
+            for (int m = 0; m <= p; ++m) {
+                if (m == b) continue;
+                double term = 1.0 / (R->xi[b] - R->xi[m]);
+                for (int l = 0; l <= p; ++l) {
+                    if (l == b || l == m) continue;
+                    term *= (R->xi[a] - R->xi[l]) / (R->xi[b] - R->xi[l]);
+                }
+                s += term;
+            }
+            R->D[a][b] = s;
+        }
+    return 0;
+}
+
+/* ---- problem ---- */
+typedef struct {
+    int dim, nx, ny, p, n, np1, ndir, G, nbnode;
+    double hx, hy;
+    const double *omega, *w, *sigma, *q, *inflow;
+    double inv_c_dt;
+    refel R;
+} prob;
+
+static int bnode(const prob *P, int face, int idx, int node) {
+    /* face 0:x- 1:x+ 2:y- 3:y+ ; idx = j (x faces) or i (y faces); node = b or a */
+    if (P->dim == 1) return face;  /* [x=0, x=1] */
+    int np1 = P->np1;
+    switch (face) {
+        case 0: return idx * np1 + node;
+        case 1: return P->ny * np1 + idx * np1 + node;
+        case 2: return 2 * P->ny * np1 + idx * np1 + node;
+        default: return 2 * P->ny * np1 + P->nx * np1 + idx * np1 + node;
+    }
+}
+
+/* Solve A x = r (n x n, row-major, destroyed) by LU with partial pivoting. */
+static int lu_solve(int n, double *A, double *r, double *x) {
+    int piv[MAXN];
+    for (int k = 0; k < n; ++k) piv[k] = k;
+    for (int k = 0; k < n; ++k) {
+        int pr = k;
+        double best = fabs(A[k * n + k]);
+        for (int i = k + 1; i < n; ++i)
+            if (fabs(A[i * n + k]) > best) { best = fabs(A[i * n + k]); pr = i; }
+        if (best == 0.0) return -1;
+        if (pr != k) {
+            for (int j = 0; j < n; ++j) { double t = A[k * n + j]; A[k * n + j] = A[pr * n + j]; A[pr * n + j] = t; }
+            double t = r[k]; r[k] = r[pr]; r[pr] = t;
+        }
+        for (int i = k + 1; i < n; ++i) {
+            double f = A[i * n + k] / A[k * n + k];
+            A[i * n + k] = 0.0;
+            for (int j = k + 1; j < n; ++j) A[i * n + j] -= f * A[k * n + j];
+            r[i] -= f * r[k];
+        }
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = r[i];
+        for (int j = i + 1; j < n; ++j) s -= A[i * n + j] * x[j];
+        x[i] = s / A[i * n + i];
+    }
+    return 0;
+}
+
+/*
+ * One (d,g) sweep.  psi [N_el][n].  Returns 0, or -1 on a singular block.
+ * Weak form per element K, test function l_k (eq:dgsn_transport with the
+ * upwind flux):
+ *   - int_K Omega.grad(l_k) psi + sum_faces int_f (Omega.n) l_k psi^ + int_K sigma~ l_k psi = int_K l_k q
+ * psi^ = own trace on outflow faces (Omega.n > 0), the upwind neighbour's
+ * coincident trace or the prescribed inflow on inflow faces (Omega.n < 0).
+ * GLL lumping: int_K f = sum_l W_l f(x_l), W_l = hx hy wh_a wh_b;
+ * int_f f = sum over face nodes of (face weight) f; grad l_k at node l =
+ * (D_{a_l a_k}/hx delta_{b_k b_l}, D_{b_l b_k}/hy delta_{a_k a_l}).
+ */
+static int sweep_dg(const prob *P, int d, int g, double *psi) {
+    const int nx = P->nx, ny = P->ny, np1 = P->np1, n = P->n, G = P->G;
+    const double ox = P->omega[3 * d + 0], oy = (P->dim == 2) ? P->omega[3 * d + 1] : 0.0;
+    const double hx = P->hx, hy = P->hy;
+    const refel *R = &P->R;
+    const int i0 = (ox >= 0.0) ? 0 : nx - 1, di = (ox >= 0.0) ? 1 : -1;
+    const int j0 = (oy >= 0.0) ? 0 : ny - 1, dj = (oy >= 0.0) ? 1 : -1;
+    double A[MAXN * MAXN], r[MAXN], x[MAXN];
+    double W[MAXN];
+    int ak[MAXN], bk[MAXN];
+    for (int k = 0; k < n; ++k) {
+        ak[k] = k % np1;
+        bk[k] = (P->dim == 2) ? k / np1 : 0;
+        W[k] = (P->dim == 2) ? hx * hy * R->wh[ak[k]] * R->wh[bk[k]] : hx * R->wh[ak[k]];
+    }
+    for (int jj = 0; jj < ny; ++jj) {
+        const int j = j0 + dj * jj;
+        for (int ii = 0; ii < nx; ++ii) {
+            const int i = i0 + di * ii;
+            const int e = i + nx * j;
+            const double sig_t = P->sigma[(size_t)e * G + g] + P->inv_c_dt;
+            memset(A, 0, sizeof(A));
+            for (int k = 0; k < n; ++k) {
+                /* mass: int sigma~ l_k psi ;  source: int l_k q */
+                A[k * n + k] += sig_t * W[k];
+                r[k] = W[k] * P->q[((size_t)e * n + k) * G + g];
+                /* streaming: - int Omega.grad(l_k) psi = - sum_l W_l Omega.grad l_k(x_l) psi_l */
+                for (int l = 0; l < n; ++l) {
+                    double gx = (bk[k] == bk[l]) ? R->D[ak[l]][ak[k]] / hx : 0.0;
+                    double gy = (P->dim == 2 && ak[k] == ak[l]) ? R->D[bk[l]][bk[k]] / hy : 0.0;
+                    A[k * n + l] -= W[l] * (ox * gx + oy * gy);
+                }
+            }
+            /* faces: (normal component, node-on-face test, face weight, upwind value) */
+            const int nfaces = (P->dim == 2) ? 4 : 2;
+            for (int f = 0; f < nfaces; ++f) {
+                double on;  /* Omega . n_f */
+                switch (f) {
+                    case 0: on = -ox; break;
+                    case 1: on = ox; break;
+                    case 2: on = -oy; break;
+                    default: on = oy; break;
+                }
+                if (on == 0.0) continue;  /* R15: no face term */
+                for (int k = 0; k < n; ++k) {
+                    int onface;
+                    double wf;
+                    switch (f) {
+                        case 0: onface = (ak[k] == 0); wf = (P->dim == 2) ? hy * R->wh[bk[k]] : 1.0; break;
+                        case 1: onface = (ak[k] == np1 - 1); wf = (P->dim == 2) ? hy * R->wh[bk[k]] : 1.0; break;
+                        case 2: onface = (bk[k] == 0); wf = hx * R->wh[ak[k]]; break;
+                        default: onface = (bk[k] == np1 - 1); wf = hx * R->wh[ak[k]]; break;
+                    }
+                    if (!onface) continue;
+                    if (on > 0.0) {
+                        A[k * n + k] += on * wf;  /* outflow: own trace */
+                    } else {
+                        double up;
+                        int ni = i, nj = j, nk;
+                        switch (f) {
+                            case 0: ni = i - 1; nk = (np1 - 1) + np1 * bk[k]; break;
+                            case 1: ni = i + 1; nk = 0 + np1 * bk[k]; break;
+                            case 2: nj = j - 1; nk = ak[k] + np1 * (np1 - 1); break;
+                            default: nj = j + 1; nk = ak[k]; break;
+                        }
+                        if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) {
+                            int idx = (f < 2) ? j : i;
+                            int node = (f < 2) ? bk[k] : ak[k];
+                            up = P->inflow[(size_t)bnode(P, f, idx, node) * G + g];
+                        } else {
+                            if (P->dim == 1) nk = (f == 0) ? np1 - 1 : 0;
+                            up = psi[(size_t)(ni + nx * nj) * n + nk];
+                        }
+                        r[k] += (-on) * wf * up;  /* inflow: upwind trace */
+                    }
+                }
+            }
+            if (lu_solve(n, A, r, x) != 0) return -1;
+            for (int k = 0; k < n; ++k) psi[(size_t)e * n + k] = x[k];
+        }
+    }
+    return 0;
+}
+
+/* ---- Neumaier-compensated accumulator ---- */
+static inline void nadd(double *s, double *c, double v) {
+    double t = *s + v;
+    if (fabs(*s) >= fabs(v)) *c += (*s - t) + v;
+    else *c += (v - t) + *s;
+    *s = t;
+}
+
+static int setup(prob *P, int dim, int nx, int ny, double lx, double ly, int p, int ndir,
+                 const double *omega, const double *w, int G, const double *sigma, double inv_c_dt,
+                 const double *q, const double *inflow) {
+    if (dim != 1 && dim != 2) return -2;
+    if (make_refel(p, &P->R) != 0) return -2;
+    if (nx <= 0 || (dim == 2 && ny <= 0) || ndir <= 0 || G <= 0 || lx <= 0.0) return -2;
+    P->dim = dim; P->nx = nx; P->ny = (dim == 2) ? ny : 1; P->p = p; P->np1 = p + 1;
+    P->n = (dim == 2) ? (p + 1) * (p + 1) : p + 1;
+    P->ndir = ndir; P->G = G;
+    P->nbnode = (dim == 1) ? 2 : 2 * (nx + ny) * (p + 1);
+    P->hx = lx / nx; P->hy = (dim == 2) ? ly / ny : 1.0;
+    P->omega = omega; P->w = w; P->sigma = sigma; P->q = q; P->inflow = inflow;
+    P->inv_c_dt = inv_c_dt;
+    return 0;
+}
+
+/* number of output doubles: phi, J(dim), T(1 or 3) per node; beta, J+ per boundary node */
+static size_t out_size(const prob *P, size_t *nodes, int *nT) {
+    *nodes = (size_t)P->nx * P->ny * P->n;
+    *nT = (P->dim == 1) ? 1 : 3;
+    return (*nodes) * (1 + P->dim + *nT) + 2 * (size_t)P->nbnode;
+}
+
+int oracle_out_size(int dim, int nx, int ny, int p) {
+    int n = (dim == 2) ? (p + 1) * (p + 1) : p + 1;
+    int nel = (dim == 2) ? nx * ny : nx;
+    int nT = (dim == 1) ? 1 : 3;
+    int nb = (dim == 1) ? 2 : 2 * (nx + ny) * (p + 1);
+    return nel * n * (1 + dim + nT) + 2 * nb;
+}
+
+/* alpha_n = sum_d w_d |Omega_d . n| / sum_d w_d for n in {x-, x+, y-, y+} (eq:alpha) */
+void oracle_alpha(int dim, int ndir, const double *omega, const double *w, double *alpha4) {
+    double sw = 0.0, sx = 0.0, sy = 0.0;
+    for (int d = 0; d < ndir; ++d) {
+        sw += w[d];
+        sx += w[d] * fabs(omega[3 * d]);
+        sy += w[d] * ((dim == 2) ? fabs(omega[3 * d + 1]) : 0.0);
+    }
+    alpha4[0] = alpha4[1] = sx / sw;
+    alpha4[2] = alpha4[3] = sy / sw;
+}
+
+/* psi for a single (d,g): psi_out [N_el][n].  0 = ok. */
+int oracle_sweep_psi(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
+                     const double *omega, const double *w, int G, const double *sigma,
+                     double inv_c_dt, const double *q, const double *inflow, int d, int g,
+                     double *psi_out) {
+    prob P;
+    int rc = setup(&P, dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, inv_c_dt, q, inflow);
+    if (rc) return rc;
+    if (d < 0 || d >= ndir || g < 0 || g >= G) return -2;
+    return sweep_dg(&P, d, g, psi_out);
+}
+
+/*
+ * Full sweep + gray moments.  out layout (packed, as the C-ABI's closures_get):
+ *   phi[N_el][n] | J[dim][N_el][n] | T[nT][N_el][n] | beta[N_bnode] | Jplus[N_bnode]
+ * nthreads <= 0: OpenMP default.  Returns 0, -1 singular block, -2 bad args, -3 OOM.
+ */
+int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
+                 const double *omega, const double *w, int G, const double *sigma,
+                 double inv_c_dt, const double *q, const double *inflow, double *out,
+                 int nthreads) {
+    prob P;
+    int rc = setup(&P, dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, inv_c_dt, q, inflow);
+    if (rc) return rc;
+    size_t nodes;
+    int nT;
+    const size_t nout = out_size(&P, &nodes, &nT);
+    const int ncomp = 1 + dim + nT;
+
+    /* per-direction closure coefficients, precomputed as w (Omega Omega - I/3) (R16) */
+    double *coef = (double *)malloc(sizeof(double) * (size_t)ndir * 6);
+    if (!coef) return -3;
+    for (int d = 0; d < ndir; ++d) {
+        const double wd = w[d], ox = omega[3 * d], oy = (dim == 2) ? omega[3 * d + 1] : 0.0;
+        double *c = coef + 6 * d;
+        c[0] = wd;
+        if (dim == 1) {
+            c[1] = wd * ox;
+            c[2] = wd * (ox * ox - 1.0 / 3.0);
+        } else {
+            c[1] = wd * ox;
+            c[2] = wd * oy;
+            c[3] = wd * (ox * ox - 1.0 / 3.0);
+            c[4] = wd * (ox * oy);
+            c[5] = wd * (oy * oy - 1.0 / 3.0);
+        }
+    }
+    double alpha4[4];
+    oracle_alpha(dim, ndir, omega, w, alpha4);
+
+    /* boundary face nodes: element, node, face */
+    const int nb = P.nbnode;
+    int *b_el = (int *)malloc(sizeof(int) * nb), *b_k = (int *)malloc(sizeof(int) * nb), *b_f = (int *)malloc(sizeof(int) * nb);
+    if (!b_el || !b_k || !b_f) { free(coef); free(b_el); free(b_k); free(b_f); return -3; }
+    if (dim == 1) {
+        b_el[0] = 0; b_k[0] = 0; b_f[0] = 0;
+        b_el[1] = nx - 1; b_k[1] = P.np1 - 1; b_f[1] = 1;
+    } else {
+        const int np1 = P.np1;
+        for (int j = 0; j < P.ny; ++j)
+            for (int b = 0; b < np1; ++b) {
+                int t = bnode(&P, 0, j, b); b_el[t] = 0 + nx * j; b_k[t] = 0 + np1 * b; b_f[t] = 0;
+                t = bnode(&P, 1, j, b); b_el[t] = (nx - 1) + nx * j; b_k[t] = (np1 - 1) + np1 * b; b_f[t] = 1;
+            }
+        for (int i = 0; i < nx; ++i)
+            for (int a = 0; a < np1; ++a) {
+                int t = bnode(&P, 2, i, a); b_el[t] = i; b_k[t] = a; b_f[t] = 2;
+                t = bnode(&P, 3, i, a); b_el[t] = i + nx * (P.ny - 1); b_k[t] = a + np1 * (np1 - 1); b_f[t] = 3;
+            }
+    }
+
+    int nth = 1;
+#ifdef _OPENMP
+    nth = (nthreads > 0) ? nthreads : omp_get_max_threads();
+#endif
+    const long npairs = (long)ndir * G;
+    if (nth > npairs) nth = (int)npairs;
+    if (nth < 1) nth = 1;
+    double *acc = (double *)calloc((size_t)nth * nout * 2, sizeof(double));
+    if (!acc) { free(coef); free(b_el); free(b_k); free(b_f); return -3; }
+    int fail = 0;
+
+#pragma omp parallel num_threads(nth)
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        double *S = acc + (size_t)tid * nout * 2;  /* sums */
+        double *C = S + nout;                      /* compensations */
+        double *psi = (double *)malloc(sizeof(double) * nodes);
+        if (!psi) {
+#pragma omp atomic write
+            fail = -3;
+        }
+#pragma omp for schedule(static)
+        for (long pr = 0; pr < npairs; ++pr) {
+            if (!psi) continue;
+            const int d = (int)(pr / G), g = (int)(pr % G);
+            if (sweep_dg(&P, d, g, psi) != 0) {
+#pragma omp atomic write
+                fail = -1;
+                continue;
+            }
+            const double *c = coef + 6 * d;
+            for (size_t v = 0; v < nodes; ++v) {
+                const double ps = psi[v];
+                for (int m = 0; m < ncomp; ++m) nadd(&S[m * nodes + v], &C[m * nodes + v], c[m] * ps);
+            }
+            const double ox = omega[3 * d], oy = (dim == 2) ? omega[3 * d + 1] : 0.0;
+            for (int t = 0; t < nb; ++t) {
+                double on;
+                switch (b_f[t]) {
+                    case 0: on = -ox; break;
+                    case 1: on = ox; break;
+                    case 2: on = -oy; break;
+                    default: on = oy; break;
+                }
+                const double ps = psi[(size_t)b_el[t] * P.n + b_k[t]];
+                const size_t ib = (size_t)ncomp * nodes + t, ij = ib + nb;
+                nadd(&S[ib], &C[ib], w[d] * (fabs(on) - alpha4[b_f[t]]) * ps);
+                if (on > 0.0) nadd(&S[ij], &C[ij], w[d] * on * ps);
+            }
+        }
+        free(psi);
+    }
+    if (!fail) {
+        for (size_t v = 0; v < nout; ++v) {
+            double s = 0.0, c = 0.0;
+            for (int t = 0; t < nth; ++t) {
+                const double *S = acc + (size_t)t * nout * 2;
+                nadd(&s, &c, S[v]);
+                nadd(&s, &c, S[nout + v]);
+            }
+            out[v] = s + c;
+        }
+    }
+    free(acc); free(coef); free(b_el); free(b_k); free(b_f);
+    return fail;
+}
