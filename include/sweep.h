@@ -1,0 +1,153 @@
+/*
+ * sweep.h — C ABI of libsweep.so: the B200 (sm_100a) DG S_N transport sweep
+ * fused with the gray Second-Moment closures of arXiv 2504.21784.
+ *
+ * What one sweep_run computes (PAPER.md = /root/reference/PAPER.md):
+ *   For every direction d of the quadrature set and every local group g,
+ *   psi_{d,g} in Y_p (discontinuous, tensor GLL nodal basis of order p) is the
+ *   solution of the lumped upwind-DG weak form (eq:dgsn_transport,
+ *   PAPER.md:332-336, upwind flux PAPER.md:299-327, GLL lumping PAPER.md:654)
+ *   of the backward-Euler transport equation (eq:smm_be_transport)
+ *       Omega_d . grad psi + (sigma_t,g + 1/(c dt)) psi = q_g
+ *   with a GIVEN isotropic nodal source q (each high-order solve "inverts the
+ *   left hand side ... only") and the prescribed isotropic inflow
+ *   on inflow faces.  psi is never stored; the library
+ *   returns only the gray sums over all directions and groups
+ *       phi  = sum_g sum_d w_d psi                     (c E,   PAPER.md:156-158)
+ *       J    = sum_g sum_d w_d Omega_d psi             (F,     PAPER.md:160-161)
+ *       T    = sum_g sum_d w_d (Omega_d Omega_d - I/3) psi
+ *       beta = sum_g sum_d w_d (|Omega_d . n| - alpha_n) psi
+ *       J+   = sum_g sum_{Omega_d.n > 0} w_d (Omega_d . n) psi
+ *   with alpha_n = sum_d w_d |Omega_d . n| / sum_d w_d  (eq:alpha),
+ *   beta and J+ on every boundary face node, using the element's own nodal
+ *   trace for every direction (reading R5).
+ *
+ * Mesh: uniform Cartesian, dim 1 (slab [0,lx], nx elements) or 2 ([0,lx]x[0,ly],
+ * nx*ny quads).  Element e = i + nx*j.  Node k = a + (p+1)*b (a: x index,
+ * b: y index) at the GLL points of the element; n = (p+1)^dim.
+ * Boundary face nodes, in this order: face x- (j = 0..ny-1, b = 0..p),
+ * x+ (j, b), y- (i = 0..nx-1, a = 0..p), y+ (i, a); a corner node appears once
+ * per face (reading R18).  dim 1: [x = 0, x = lx].  N_bnode = 2 (dim 1) or
+ * 2 (nx + ny)(p + 1).
+ *
+ * Output packing (doubles), all gray = summed over every group of every rank:
+ *   phi[N_el][n] | J[dim][N_el][n] | T[nT][N_el][n] | beta[N_bnode] | Jplus[N_bnode]
+ *   nT = 1 (dim 1: T_xx) or 3 (dim 2: T_xx, T_xy, T_yy; T_zz = -T_xx - T_yy).
+ *
+ * Every function returns an int status (SWEEP_OK = 0) and never aborts or
+ * throws across the ABI; sweep_last_error gives the message of the last
+ * failure on a handle.  A handle is not re-entrant; separate handles may be
+ * used from separate threads/streams.  Each call sets the handle's device and
+ * restores the caller's current device before returning.
+ */
+#ifndef PAPER_2504_21784_B200_SWEEP_H
+#define PAPER_2504_21784_B200_SWEEP_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SWEEP_OK = 0,
+    SWEEP_E_ARG = 1,      /* null pointer, dim not in {1,2}, p not in {1,2}, sizes <= 0, lx/ly <= 0 */
+    SWEEP_E_QUAD = 2,     /* |sum w - 1| > 1e-13, w_d <= 0, |Omega_d| != 1 (dim 2) or |mu| > 1 (dim 1) */
+    SWEEP_E_SIGMA = 3,    /* sigma_t + 1/(c dt) <= 0 or non-finite sigma, or a non-finite result
+                             (non-finite q / inflow); detected on the device, reported by closures_get */
+    SWEEP_E_CUDA = 4,     /* CUDA error (message via sweep_last_error) */
+    SWEEP_E_NCCL = 5,     /* NCCL missing or failed */
+    SWEEP_E_INTERNAL = 6  /* setup self-check failed (e.g. eigen-decomposition residual) */
+};
+
+/* flags */
+#define SWEEP_FOLD_Z 1u          /* dim 2: sweep each pair of directions with identical (Omega_x, Omega_y)
+                                    (e.g. +-Omega_z) once with the summed weight; exact (reading R20) */
+#define SWEEP_DETERMINISTIC 2u   /* accepted for API compatibility: every reduction already runs in a
+                                    fixed order, so results are bitwise repeatable in all modes */
+
+typedef struct sweep_handle sweep_handle;   /* opaque, owned by the library */
+
+typedef struct {
+    int dim;                 /* 1 or 2 */
+    int nx, ny;              /* elements per axis; ny ignored (treated as 1) for dim 1 */
+    double lx, ly;           /* domain lengths (> 0); ly ignored for dim 1 */
+    int p;                   /* DG order: 1 (paper) or 2 (reading R1) */
+    int n_dir;               /* number of directions */
+    const double *omega;     /* HOST [n_dir][3] unit vectors (dim 1: omega[d][0] = mu_d); copied at setup */
+    const double *w;         /* HOST [n_dir] weights, sum = 1 (+-1e-13), each > 0; copied at setup */
+    int n_group_local;       /* groups held by this rank (G_loc >= 1) */
+    int group_offset;        /* first global group index of this rank (informational) */
+    int n_group_total;       /* total groups over all ranks (informational) */
+    int device;              /* CUDA device ordinal */
+    int nranks, rank;        /* nranks = 1: no collective; > 1: NCCL all-reduce of the gray output */
+    const void *nccl_id;     /* 128-byte ncclUniqueId created by rank 0 and broadcast (nranks > 1), else NULL */
+    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC */
+} sweep_desc;
+
+/* Validate the description, fold/sort directions into sweep quadrants,
+ * precompute per-direction tables (a1) and the wavefront schedule (a2),
+ * allocate device workspace and, for nranks > 1, initialise the NCCL
+ * communicator (ncclCommInitRank; collective over all ranks).
+ * *out receives the handle, or NULL on failure. */
+int sweep_setup(const sweep_desc *desc, sweep_handle **out);
+
+/* Offsets (in doubles) of phi, J, T, beta, Jplus inside the packed output,
+ * and its total length. */
+int sweep_layout(const sweep_handle *h, size_t off[5], size_t *total_doubles);
+
+/* One sweep + fused closures, enqueued asynchronously on cuda_stream
+ * (a cudaStream_t; NULL = legacy default stream).  Device pointers, borrowed,
+ * must stay valid and unmodified until the stream work completes:
+ *   d_sigma  [N_el][G_loc]       sigma_t,g per element (piecewise constant)
+ *   d_q      [N_el][n][G_loc]    nodal isotropic source q_g (reading R2: no 1/(4 pi))
+ *   d_inflow [N_bnode][G_loc]    isotropic inflow per boundary face node (0 = vacuum)
+ * inv_c_dt = 1/(c dt) > 0 is added to sigma_t.  Group is the
+ * fastest index.  Ends with the in-place NCCL all-reduce when nranks > 1. */
+int sweep_run(sweep_handle *h, const double *d_sigma, double inv_c_dt, const double *d_q,
+              const double *d_inflow, void *cuda_stream);
+
+/* Synchronise cuda_stream, report the device error flag (SWEEP_E_SIGMA), and
+ * copy the packed gray output (n_doubles must equal the layout total) to
+ * out, which may be device or host memory (cudaMemcpyDefault). */
+int closures_get(sweep_handle *h, double *out, size_t n_doubles, void *cuda_stream);
+
+/* End-to-end convenience call with HOST buffers (pinned recommended): copies
+ * the inputs host->device into library-owned buffers, runs the sweep, copies
+ * the packed output device->host and synchronises.  Same shapes as sweep_run. */
+int sweep_run_host(sweep_handle *h, const double *h_sigma, double inv_c_dt, const double *h_q,
+                   const double *h_inflow, double *h_out, size_t n_doubles, void *cuda_stream);
+
+/* Statistics of the last sweep_run: number of kernels launched (out[0]),
+ * distinct directions swept (out[1], after folding), work streams (out[2]),
+ * persistent CTAs (out[3]). */
+int sweep_stats(const sweep_handle *h, long long out[4]);
+
+/* Per-run kernel timing (CUDA events recorded on the run's stream around the
+ * sweep kernel, the finalize kernel and the all-reduce).  enable != 0 clears
+ * and starts recording (ring of the last 1024 runs); 0 stops. */
+int sweep_timing(sweep_handle *h, int enable);
+
+/* Durations (ms) of the recorded runs, oldest first: ms[3*r + 0] sweep kernel,
+ * [3*r + 1] finalize kernel, [3*r + 2] all-reduce (0 when nranks = 1).
+ * Synchronises on the recorded events; *n_runs receives the count (<= max_runs). */
+int sweep_kernel_times(sweep_handle *h, double *ms, int max_runs, int *n_runs);
+
+/* Measure the device's FP64 FMA throughput (TFLOP/s) with a dependent-chain-free
+ * DFMA kernel on every SM (roofline denominator). */
+int sweep_fp64_probe(int device, double *tflops);
+
+/* Fill out128 with a fresh 128-byte ncclUniqueId (rank 0 calls this, then
+ * broadcasts it to the other ranks, e.g. with torch.distributed). */
+int sweep_nccl_unique_id(void *out128);
+
+/* Free every device and host resource of the handle (and the NCCL comm). */
+void sweep_destroy(sweep_handle *h);
+
+/* Message of the last failure on h ("" if none); h may be NULL for setup failures. */
+const char *sweep_last_error(const sweep_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,89 @@
+// sweep_internal.h — data shared between the host setup (sweep_host.cpp) and
+// the sm_100a kernels (sweep_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace sweepk {
+
+// Per (folded) direction, in sweep coordinates (every direction is mapped to
+// the (+,+) quadrant by mirroring the element order and the nodes).
+struct DirConst {
+    double cx, cy;     // |Omega_x|/hx, |Omega_y|/hy   (1-D: cx = |mu|/h, cy = 0)
+    double mom[6];     // moment weights with the SIGNED direction:
+                       //  2-D: w, w Ox, w Oy, w(Ox^2-1/3), w Ox Oy, w(Oy^2-1/3)
+                       //  1-D: w, w mu, w(mu^2-1/3), 0, 0, 0
+    double bw[4];      // beta weights per physical face x-,x+,y-,y+: w(|Omega.n| - alpha_n)
+    double jw[4];      // J+ weights per physical face: w max(Omega.n, 0)
+};
+
+// One work stream = (quadrant, group block, direction set): the lanes of one CTA.
+struct StreamDesc {
+    int quadrant;      // 2-D: bit0 = (Omega_x < 0), bit1 = (Omega_y < 0); 1-D: bit0 = (mu < 0)
+    int g0, ng;        // local groups [g0, g0+ng)
+    int d0, nd;        // directions [d0, d0+nd) of the quadrant-sorted table
+};
+
+// Modal constants of the p = 2 reference operator A^ = V Lambda W (W = V^-1),
+// A^ = [[3,4,-1],[-1,0,1],[1,-4,3]] (derived in DESIGN.md §4 from the lumped
+// weak form).  Mode 0 real (lambda0), mode 1 = mu + i nu, mode 2 = conj.
+struct ModalConsts {
+    double lam0, mu, nu;
+    double W0[3];          // real row of W
+    double W1re[3], W1im[3];
+    double V0[3];          // real column of V (V[a][0])
+    double V1re[3], V1im[3];   // V[a][1]
+    // real 9x9 maps between nodal (k = a + 3b, sweep coordinates) and the 9 modal
+    // reals m = [u00, u01r, u01i, u10r, u10i, u11r, u11i, u12r, u12i]
+    double fwd[9][9];      // modal = fwd * nodal   (W (x) W)
+    double bck[9][9];      // nodal = bck * modal   (V (x) V)
+};
+
+struct Sweep2DParams {
+    int nx, ny, G;                 // G = groups on this rank
+    int n_streams, n_strips, n_chunks, n_tasks;
+    int gb;                        // lanes per direction (power of 2)
+    int dset;                      // directions per CTA
+    int nbnode;
+    double inv_c_dt;
+    const double* sigma;           // [N_el][G]
+    const double* q;               // [N_el][n][G]
+    const double* inflow;          // [N_bnode][G]
+    const DirConst* dirs;          // quadrant-sorted
+    const StreamDesc* streams;
+    int* progress;                 // [n_streams][n_strips] chunks completed
+    int* task_counter;
+    double* ytr;                   // [n_streams][2][nx][NT][NL]
+    double* slabs;                 // [n_streams][out_size]
+    size_t out_size;
+    size_t nodes;                  // N_el * n
+    int* err;
+};
+
+struct Sweep1DParams {
+    int nx, G, n_streams, gb, nseg, seglen;
+    double inv_c_dt;
+    const double* sigma;
+    const double* q;
+    const double* inflow;
+    const DirConst* dirs;
+    const StreamDesc* streams;
+    double* slabs;
+    size_t out_size;
+    size_t nodes;
+    int* err;
+};
+
+// launchers (sweep_kernels.cu); return cudaError_t as int
+int upload_modal(const ModalConsts& mc);
+int launch_sweep2d(int p, int log2gb, const Sweep2DParams& prm, int grid, int block, size_t smem, void* stream);
+int launch_sweep1d(int p, int log2gb, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream);
+int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream);
+int sweep2d_smem_bytes(int p, int gb, int dset);
+int sweep2d_occupancy(int p, int log2gb, int block, size_t smem, int* blocks_per_sm);
+int sweep2d_rows_per_strip(int p);
+int sweep2d_cols_per_chunk(int p);
+const char* cuda_err_string(int e);
+int fp64_probe(int device, double* tflops);
+
+}  // namespace sweepk

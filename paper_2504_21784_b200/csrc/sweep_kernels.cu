@@ -1,0 +1,837 @@
+// sweep_kernels.cu — sm_100a kernels of the fused DG S_N sweep + gray SM closures.
+//
+// Method: for each direction d and group g the lumped upwind-DG
+// element system (eq:dgsn_transport PAPER.md:332-336, GLL lumping :654) is
+// solved element by element in upwind order (upwind flux :299-327), and the
+// gray moments phi, J, T, beta, J+  are accumulated on the
+// fly; psi never leaves registers / shared memory.
+//
+// Design:
+//  * every direction is handled in "sweep coordinates": its quadrant's axes are
+//    mirrored so that it streams in +x,+y; the element operator then is
+//    sigma~ I + cx A^(x) + cy A^(y), cx = |Omega_x|/hx, cy = |Omega_y|/hy, with the
+//    SAME reference matrix A^ for all directions;
+//  * p = 1: closed-form inverse of the 4x4 Kronecker sum (one reciprocal);
+//  * p = 2: A^ = V Lambda W is diagonalised once; q is transformed per
+//    (element, group) in shared memory and shared by every direction of the
+//    CTA, traces travel in modal form, and the solve is a diagonal scaling
+//    (one reciprocal for five denominators, Montgomery's trick);
+//  * 2-D schedule: a strip pipeline — one CTA owns a strip of T element rows
+//    for one (quadrant, group block, direction set) and walks it left to right
+//    in chunks of C columns; the strip above waits on a per-chunk progress flag
+//    (release/acquire) and reads the strip's top traces from a 2-slot ring;
+//    persistent CTAs claim strips in topological order (deadlock free);
+//  * lanes = (direction, group); the group sum is a warp reduce-scatter, the
+//    direction sum with the moment weights is done per chunk in shared memory,
+//    and each CTA writes its partial gray fields to its own slab, summed in a
+//    fixed order by finalize (deterministic).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sweep_internal.h"
+
+namespace sweepk {
+
+__constant__ ModalConsts cM;
+
+#define FULLMASK 0xffffffffu
+
+// 1/x: MUFU.RCP64H seed + one cubic Newton step (relative error ~e^3 of the seed).
+__device__ __forceinline__ double rcp64(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, fma(e, e, e), y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool bad_sigma(double st) { return !(st > 0.0) || !(st < 1.0e300); }
+
+// Reduce-scatter of NV doubles over the lanes selected by MASK, MASK/2, ..., 1.
+// Each stage halves the slots a lane holds; `nvalid` tracks how many of the
+// lane's slots are real (not padding), so padded slots never reach the sink.
+// On exit the sink receives (index, value) for the slots this lane owns.
+template <int NV, int MASK>
+struct ReduceScatter {
+    template <typename Sink>
+    static __device__ __forceinline__ void run(const double (&v)[NV], int lane, int idx, int nvalid, Sink& sink) {
+        if constexpr (MASK == 0) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+                if (k < nvalid) sink(idx + k, v[k]);
+        } else if constexpr (NV == 1) {
+            double o[1];
+            o[0] = v[0] + __shfl_xor_sync(FULLMASK, v[0], MASK);
+            ReduceScatter<1, MASK / 2>::run(o, lane, idx, (lane & MASK) ? 0 : nvalid, sink);
+        } else {
+            constexpr int H = (NV + 1) / 2;
+            const bool up = (lane & MASK) != 0;
+            double o[H];
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double lo = v[k];
+                const double hi = (k + H < NV) ? v[k + H] : 0.0;
+                const double send = up ? lo : hi;
+                const double keep = up ? hi : lo;
+                o[k] = keep + __shfl_xor_sync(FULLMASK, send, MASK);
+            }
+            const int nv = up ? max(0, nvalid - H) : min(H, nvalid);
+            ReduceScatter<H, MASK / 2>::run(o, lane, idx + (up ? H : 0), nv, sink);
+        }
+    }
+};
+
+// ------------------------------------------------------------------ 2-D, p = 2
+struct LaneP2 {
+    double lx0, lx1r, lx1i, ly0, ly1r, ly1i;   // lifts 6 cx W[.][0], 6 cy W[.][0]
+    double A00, A01, A10, A11;                 // real parts of the mode shifts
+    double I01, I10, I11, I12;                 // imaginary parts
+    double I01s, I10s, I11s, I12s;
+};
+
+__device__ __forceinline__ LaneP2 make_lane_p2(double cx, double cy) {
+    LaneP2 L;
+    const double l0 = cM.lam0, mu = cM.mu, nu = cM.nu;
+    L.lx0 = 6.0 * cx * cM.W0[0];
+    L.lx1r = 6.0 * cx * cM.W1re[0];
+    L.lx1i = 6.0 * cx * cM.W1im[0];
+    L.ly0 = 6.0 * cy * cM.W0[0];
+    L.ly1r = 6.0 * cy * cM.W1re[0];
+    L.ly1i = 6.0 * cy * cM.W1im[0];
+    L.A00 = (cx + cy) * l0;
+    L.A01 = cx * l0 + cy * mu;
+    L.A10 = cx * mu + cy * l0;
+    L.A11 = (cx + cy) * mu;
+    L.I01 = cy * nu;
+    L.I10 = cx * nu;
+    L.I11 = (cx + cy) * nu;
+    L.I12 = (cx - cy) * nu;
+    L.I01s = L.I01 * L.I01;
+    L.I10s = L.I10 * L.I10;
+    L.I11s = L.I11 * L.I11;
+    L.I12s = L.I12 * L.I12;
+    return L;
+}
+
+// modal element solve: u = (sigma~ + cx lam_a + cy lam_b)^-1 (q^ + lifts), and the
+// outflow traces in modal form (x+ face: y-modal, y+ face: x-modal).
+__device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const double (&qh)[9], const double (&tx)[3],
+                                         const double (&ty)[3], double (&u)[9], double (&txo)[3], double (&tyo)[3]) {
+    const double r00 = qh[0] + L.lx0 * tx[0] + L.ly0 * ty[0];
+    const double r01r = qh[1] + L.lx0 * tx[1] + L.ly1r * ty[0];
+    const double r01i = qh[2] + L.lx0 * tx[2] + L.ly1i * ty[0];
+    const double r10r = qh[3] + L.lx1r * tx[0] + L.ly0 * ty[1];
+    const double r10i = qh[4] + L.lx1i * tx[0] + L.ly0 * ty[2];
+    const double r11r = qh[5] + L.lx1r * tx[1] - L.lx1i * tx[2] + L.ly1r * ty[1] - L.ly1i * ty[2];
+    const double r11i = qh[6] + L.lx1r * tx[2] + L.lx1i * tx[1] + L.ly1r * ty[2] + L.ly1i * ty[1];
+    const double r12r = qh[7] + L.lx1r * tx[1] + L.lx1i * tx[2] + L.ly1r * ty[1] + L.ly1i * ty[2];
+    const double r12i = qh[8] + L.lx1i * tx[1] - L.lx1r * tx[2] + L.ly1r * ty[2] - L.ly1i * ty[1];
+
+    const double d00 = st + L.A00;
+    const double e01 = st + L.A01, m01 = fma(e01, e01, L.I01s);
+    const double e10 = st + L.A10, m10 = fma(e10, e10, L.I10s);
+    const double e11 = st + L.A11;
+    const double e11s = e11 * e11;
+    const double m11 = e11s + L.I11s, m12 = e11s + L.I12s;
+    // one reciprocal for the five real denominators
+    const double p1 = d00 * m01, p2 = p1 * m10, p3 = p2 * m11, p4 = p3 * m12;
+    double inv = rcp64(p4);
+    const double i12 = inv * p3;
+    inv *= m12;
+    const double i11 = inv * p2;
+    inv *= m11;
+    const double i10 = inv * p1;
+    inv *= m10;
+    const double i01 = inv * d00;
+    const double i00 = inv * m01;
+
+    u[0] = r00 * i00;
+    u[1] = (r01r * e01 + r01i * L.I01) * i01;
+    u[2] = (r01i * e01 - r01r * L.I01) * i01;
+    u[3] = (r10r * e10 + r10i * L.I10) * i10;
+    u[4] = (r10i * e10 - r10r * L.I10) * i10;
+    u[5] = (r11r * e11 + r11i * L.I11) * i11;
+    u[6] = (r11i * e11 - r11r * L.I11) * i11;
+    u[7] = (r12r * e11 + r12i * L.I12) * i12;
+    u[8] = (r12i * e11 - r12r * L.I12) * i12;
+
+    const double v0 = cM.V0[2], vr = cM.V1re[2], vi = cM.V1im[2];
+    const double sr = u[5] + u[7], dr = u[5] - u[7];
+    const double si = u[6] + u[8], di = u[6] - u[8];
+    txo[0] = v0 * u[0] + 2.0 * (vr * u[3] - vi * u[4]);
+    txo[1] = v0 * u[1] + vr * sr - vi * si;
+    txo[2] = v0 * u[2] + vr * di + vi * dr;
+    tyo[0] = v0 * u[0] + 2.0 * (vr * u[1] - vi * u[2]);
+    tyo[1] = v0 * u[3] + vr * sr - vi * di;
+    tyo[2] = v0 * u[4] + vr * si + vi * dr;
+}
+
+// ------------------------------------------------------------------ 2-D, p = 1
+// closed-form inverse of a0 I + cx Jx + cy Jy (Jx^2 = Jy^2 = -I, K = Jx Jy):
+// (a0 - cx Jx - cy Jy)(al - be K) / (al^2 - be^2), al = a0^2 + cx^2 + cy^2, be = -2 cx cy.
+struct LaneP1 {
+    double cx, cy, cxy, sq, be, be2, lx, ly;
+};
+__device__ __forceinline__ LaneP1 make_lane_p1(double cx, double cy) {
+    LaneP1 L;
+    L.cx = cx;
+    L.cy = cy;
+    L.cxy = cx + cy;
+    L.sq = cx * cx + cy * cy;
+    L.be = -2.0 * cx * cy;
+    L.be2 = L.be * L.be;
+    L.lx = 2.0 * cx;
+    L.ly = 2.0 * cy;
+    return L;
+}
+// nodal, sweep coordinates, k = a + 2b: psi[0]=(0,0) [1]=(1,0) [2]=(0,1) [3]=(1,1)
+__device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const double (&q)[4], const double (&tx)[2],
+                                         const double (&ty)[2], double (&u)[4], double (&txo)[2], double (&tyo)[2]) {
+    const double r00 = q[0] + L.lx * tx[0] + L.ly * ty[0];
+    const double r10 = q[1] + L.ly * ty[1];
+    const double r01 = q[2] + L.lx * tx[1];
+    const double r11 = q[3];
+    const double a0 = st + L.cxy;
+    const double al = fma(a0, a0, L.sq);
+    const double det = fma(al, al, -L.be2);
+    const double inv = rcp64(det);
+    const double ai = al * inv, bi = L.be * inv;
+    const double s00 = ai * r00 - bi * r11;
+    const double s11 = ai * r11 - bi * r00;
+    const double s10 = ai * r10 + bi * r01;
+    const double s01 = ai * r01 + bi * r10;
+    u[0] = a0 * s00 - L.cx * s10 - L.cy * s01;
+    u[1] = a0 * s10 + L.cx * s00 - L.cy * s11;
+    u[2] = a0 * s01 - L.cx * s11 + L.cy * s00;
+    u[3] = a0 * s11 + L.cx * s01 + L.cy * s10;
+    txo[0] = u[1];
+    txo[1] = u[3];
+    tyo[0] = u[2];
+    tyo[1] = u[3];
+}
+
+__host__ __device__ constexpr int rows_per_strip(int P) { return P == 2 ? 4 : 8; }
+__host__ __device__ constexpr int cols_per_chunk(int P) { return 8; }
+__host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
+
+__device__ __forceinline__ int bnode2d(int face, int idx, int node, int nx, int ny, int np1) {
+    switch (face) {
+        case 0: return idx * np1 + node;
+        case 1: return ny * np1 + idx * np1 + node;
+        case 2: return 2 * ny * np1 + idx * np1 + node;
+        default: return 2 * ny * np1 + nx * np1 + idx * np1 + node;
+    }
+}
+
+template <int P, int LOG2GB>
+__global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm) {
+    constexpr int NP1 = P + 1;
+    constexpr int NN = NP1 * NP1;
+    constexpr int NQ = nq_of(P);
+    constexpr int NT = NP1;  // trace reals per face (p=2: modal 1 real + 1 complex)
+    constexpr int GB = 1 << LOG2GB;
+    constexpr int T = rows_per_strip(P);
+    constexpr int C = cols_per_chunk(P);
+    constexpr int CT = C * T;
+    constexpr int NFIELD = 14;  // 6 moments + (beta, J+) x 4 faces
+
+    const int NL = blockDim.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int gl = tid & (GB - 1);
+    const int dl = tid >> LOG2GB;
+    const int dset = NL >> LOG2GB;
+
+    extern __shared__ __align__(16) double smem[];
+    double* qs = smem;                 // [CT][NQ][GB]
+    double* ss = qs + CT * NQ * GB;    // [CT][GB]
+    double* S = ss + CT * GB;          // [CT][dset][NQ]
+    __shared__ int s_task;
+
+    const int nx = prm.nx, ny = prm.ny, G = prm.G;
+    const size_t nodes = prm.nodes;
+
+    for (;;) {
+        if (tid == 0) s_task = atomicAdd(prm.task_counter, 1);
+        __syncthreads();
+        const int task = s_task;
+        __syncthreads();
+        if (task >= prm.n_tasks) break;
+        const int J = task / prm.n_streams;
+        const int s = task - J * prm.n_streams;
+        const StreamDesc sd = prm.streams[s];
+        const bool fx = (sd.quadrant & 1) != 0, fy = (sd.quadrant & 2) != 0;
+        const bool d_on = dl < sd.nd;
+        const bool g_on = gl < sd.ng;
+        const int g = sd.g0 + gl;
+        double cx = 0.0, cy = 0.0;
+        if (d_on) {
+            cx = prm.dirs[sd.d0 + dl].cx;
+            cy = prm.dirs[sd.d0 + dl].cy;
+        }
+        const int j0 = J * T;
+        const int rows = min(T, ny - j0);
+        double* slab = prm.slabs + (size_t)s * prm.out_size;
+
+        // x-inflow traces of the strip (domain boundary at i' = 0)
+        double tx[T][NT];
+#pragma unroll
+        for (int r = 0; r < T; ++r) {
+            double t[NP1];
+#pragma unroll
+            for (int bq = 0; bq < NP1; ++bq) t[bq] = 0.0;
+            if (r < rows && g_on) {
+                const int jp = j0 + r;
+                const int j = fy ? ny - 1 - jp : jp;
+#pragma unroll
+                for (int bq = 0; bq < NP1; ++bq) {
+                    const int b = fy ? P - bq : bq;
+                    t[bq] = prm.inflow[(size_t)bnode2d(fx ? 1 : 0, j, b, nx, ny, NP1) * G + g];
+                }
+            }
+            if constexpr (P == 2) {
+                tx[r][0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
+                tx[r][1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
+                tx[r][2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
+            } else {
+                tx[r][0] = t[0];
+                tx[r][1] = t[1];
+            }
+        }
+
+        for (int c = 0; c < prm.n_chunks; ++c) {
+            const int i0 = c * C;
+            const int cols = min(C, nx - i0);
+            // ---- phase A: stage sigma~ and q (p=2: transformed to modal) for the chunk
+            for (int it = tid; it < CT * GB; it += NL) {
+                const int el = it >> LOG2GB;
+                const int gg = it & (GB - 1);
+                const int col = el / T, r = el - col * T;
+                double st = 1.0;
+                double qv[NN];
+#pragma unroll
+                for (int k = 0; k < NN; ++k) qv[k] = 0.0;
+                if (col < cols && r < rows && gg < sd.ng) {
+                    const int ip = i0 + col, jp = j0 + r;
+                    const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                    const size_t e = (size_t)i + (size_t)nx * j;
+                    const int gq = sd.g0 + gg;
+                    st = prm.sigma[e * G + gq] + prm.inv_c_dt;
+                    if (bad_sigma(st)) atomicOr(prm.err, 1);
+#pragma unroll
+                    for (int k = 0; k < NN; ++k) {
+                        const int aq = k % NP1, bq = k / NP1;
+                        const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
+                        qv[k] = prm.q[(e * NN + a + NP1 * b) * G + gq];
+                    }
+                }
+                ss[el * GB + gg] = st;
+                if constexpr (P == 2) {
+#pragma unroll
+                    for (int m = 0; m < 9; ++m) {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) acc = fma(cM.fwd[m][k], qv[k], acc);
+                        qs[(el * NQ + m) * GB + gg] = acc;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NN; ++k) qs[(el * NQ + k) * GB + gg] = qv[k];
+                }
+            }
+            // ---- wait until the strip below has finished this chunk
+            if (J > 0 && tid == 0) {
+                const int* f = prm.progress + (size_t)s * prm.n_strips + (J - 1);
+                // watchdog: a predecessor that never arrives (a bug) must not hang the GPU
+                const long long t_start = clock64();
+                while (ld_acquire(f) < c + 1) {
+                    __nanosleep(32);
+                    if (clock64() - t_start > (1LL << 34)) {
+                        atomicOr(prm.err, 4);
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+
+            // ---- phase B: sweep the chunk, column by column, rows bottom to top
+            if constexpr (P == 2) {
+                const LaneP2 L = make_lane_p2(cx, cy);
+                for (int col = 0; col < cols; ++col) {
+                    const int ip = i0 + col;
+                    double ty[NT];
+                    if (J == 0) {
+                        double t[NP1] = {0.0, 0.0, 0.0};
+                        if (g_on) {
+                            const int i = fx ? nx - 1 - ip : ip;
+#pragma unroll
+                            for (int aq = 0; aq < NP1; ++aq) {
+                                const int a = fx ? P - aq : aq;
+                                t[aq] = prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g];
+                            }
+                        }
+                        ty[0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
+                        ty[1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
+                        ty[2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
+                    } else {
+                        const double* src = prm.ytr + (((size_t)s * 2 + ((J - 1) & 1)) * nx + ip) * NT * NL;
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) ty[t] = __ldcg(src + t * NL + tid);
+                    }
+#pragma unroll
+                    for (int r = 0; r < T; ++r) {
+                        if (r < rows) {
+                            const int el = col * T + r;
+                            double qh[9], u[9], txo[3], tyo[3];
+#pragma unroll
+                            for (int m = 0; m < 9; ++m) qh[m] = qs[(el * NQ + m) * GB + gl];
+                            const double st = ss[el * GB + gl];
+                            solve_p2(L, st, qh, tx[r], ty, u, txo, tyo);
+#pragma unroll
+                            for (int t = 0; t < 3; ++t) {
+                                tx[r][t] = txo[t];
+                                ty[t] = tyo[t];
+                            }
+                            double* Sd = S + ((size_t)el * dset + dl) * NQ;
+                            auto sink = [&](int idx, double val) {
+                                if (idx < NQ) Sd[idx] = val;
+                            };
+                            ReduceScatter<9, GB / 2>::run(u, lane, 0, 9, sink);
+                        }
+                    }
+                    if (J + 1 < prm.n_strips) {
+                        double* dst = prm.ytr + (((size_t)s * 2 + (J & 1)) * nx + ip) * NT * NL;
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) __stcg(dst + t * NL + tid, ty[t]);
+                    }
+                }
+            } else {
+                const LaneP1 L = make_lane_p1(cx, cy);
+                for (int col = 0; col < cols; ++col) {
+                    const int ip = i0 + col;
+                    double ty[NT];
+                    if (J == 0) {
+                        ty[0] = ty[1] = 0.0;
+                        if (g_on) {
+                            const int i = fx ? nx - 1 - ip : ip;
+#pragma unroll
+                            for (int aq = 0; aq < NP1; ++aq) {
+                                const int a = fx ? P - aq : aq;
+                                ty[aq] = prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g];
+                            }
+                        }
+                    } else {
+                        const double* src = prm.ytr + (((size_t)s * 2 + ((J - 1) & 1)) * nx + ip) * NT * NL;
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) ty[t] = __ldcg(src + t * NL + tid);
+                    }
+#pragma unroll
+                    for (int r = 0; r < T; ++r) {
+                        if (r < rows) {
+                            const int el = col * T + r;
+                            double qn[4], u[4], txo[2], tyo[2];
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) qn[m] = qs[(el * NQ + m) * GB + gl];
+                            const double st = ss[el * GB + gl];
+                            solve_p1(L, st, qn, tx[r], ty, u, txo, tyo);
+                            tx[r][0] = txo[0];
+                            tx[r][1] = txo[1];
+                            ty[0] = tyo[0];
+                            ty[1] = tyo[1];
+                            double* Sd = S + ((size_t)el * dset + dl) * NQ;
+                            auto sink = [&](int idx, double val) {
+                                if (idx < NQ) Sd[idx] = val;
+                            };
+                            ReduceScatter<4, GB / 2>::run(u, lane, 0, 4, sink);
+                        }
+                    }
+                    if (J + 1 < prm.n_strips) {
+                        double* dst = prm.ytr + (((size_t)s * 2 + (J & 1)) * nx + ip) * NT * NL;
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) __stcg(dst + t * NL + tid, ty[t]);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                st_release(prm.progress + (size_t)s * prm.n_strips + J, c + 1);
+            }
+
+            // ---- phase C: sum over the CTA's directions with the moment / boundary
+            // weights, back to nodal values, write this stream's slab
+            for (int it = tid; it < CT * NFIELD; it += NL) {
+                const int el = it / NFIELD, f = it - el * NFIELD;
+                const int col = el / T, r = el - col * T;
+                if (col >= cols || r >= rows) continue;
+                const int ip = i0 + col, jp = j0 + r;
+                const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                int face = -1;
+                if (f >= 6) {
+                    face = (f - 6) >> 1;
+                    const bool on = (face == 0) ? (i == 0) : (face == 1) ? (i == nx - 1) : (face == 2) ? (j == 0) : (j == ny - 1);
+                    if (!on) continue;
+                }
+                double M[NQ];
+#pragma unroll
+                for (int m = 0; m < NQ; ++m) M[m] = 0.0;
+                for (int dd = 0; dd < sd.nd; ++dd) {
+                    const DirConst* D = prm.dirs + sd.d0 + dd;
+                    const double coef = (f < 6) ? __ldg(&D->mom[f]) : (((f - 6) & 1) ? __ldg(&D->jw[face]) : __ldg(&D->bw[face]));
+                    const double* Sp = S + ((size_t)el * dset + dd) * NQ;
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) M[m] = fma(coef, Sp[m], M[m]);
+                }
+                double psi[NN];
+                if constexpr (P == 2) {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 9; ++m) acc = fma(cM.bck[k][m], M[m], acc);
+                        psi[k] = acc;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) psi[k] = M[k];
+                }
+                const size_t e = (size_t)i + (size_t)nx * j;
+                if (f < 6) {
+                    double* dst = slab + (size_t)f * nodes + e * NN;
+#pragma unroll
+                    for (int k = 0; k < NN; ++k) {
+                        const int aq = k % NP1, bq = k / NP1;
+                        const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
+                        dst[a + NP1 * b] = psi[k];
+                    }
+                } else {
+                    double* dst = slab + 6 * nodes + (((f - 6) & 1) ? prm.nbnode : 0);
+#pragma unroll
+                    for (int t = 0; t < NP1; ++t) {
+                        int a, b, idx;
+                        if (face < 2) {
+                            a = (face == 0) ? 0 : P;
+                            b = t;
+                            idx = j;
+                        } else {
+                            b = (face == 2) ? 0 : P;
+                            a = t;
+                            idx = i;
+                        }
+                        const int aq = fx ? P - a : a, bq = fy ? P - b : b;
+                        dst[bnode2d(face, idx, t, nx, ny, NP1)] = psi[aq + NP1 * bq];
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 1-D
+// CTA = one stream (half-range, group block, direction set); warp w = segment
+// w of the chain; lanes = (direction, group).  The chain psi_out = t psi_in + s
+// (affine in the inflow) is solved by a segmented scan: per-segment
+// composition, a sequential pass over segments, then the final re-sweep that
+// also accumulates the moments.
+template <int P>
+__device__ __forceinline__ void solve1d(double c, double st, const double (&q)[P + 1], double up, double (&psi)[P + 1],
+                                        double& t_aff, double& s_aff) {
+    if constexpr (P == 1) {
+        const double sc = st + c;
+        const double inv = rcp64(fma(sc, sc, c * c));
+        const double r0 = fma(2.0 * c, up, q[0]);
+        psi[0] = (sc * r0 - c * q[1]) * inv;
+        psi[1] = (c * r0 + sc * q[1]) * inv;
+        t_aff = 2.0 * c * c * inv;
+        s_aff = (c * q[0] + sc * q[1]) * inv;
+    } else {
+        // modal: q^ = W q', u = (q^ + up * 6c W[:,0]) / (st + c lam)
+        const double q0 = cM.W0[0] * q[0] + cM.W0[1] * q[1] + cM.W0[2] * q[2];
+        const double q1r = cM.W1re[0] * q[0] + cM.W1re[1] * q[1] + cM.W1re[2] * q[2];
+        const double q1i = cM.W1im[0] * q[0] + cM.W1im[1] * q[1] + cM.W1im[2] * q[2];
+        const double l0 = 6.0 * c * cM.W0[0], l1r = 6.0 * c * cM.W1re[0], l1i = 6.0 * c * cM.W1im[0];
+        const double z0 = st + c * cM.lam0;
+        const double zr = st + c * cM.mu, zi = c * cM.nu;
+        const double m1 = fma(zr, zr, zi * zi);
+        const double pr = z0 * m1;
+        const double inv = rcp64(pr);
+        const double iz0 = inv * m1, im1 = inv * z0;
+        // response to the source (s) and to a unit inflow (t)
+        const double us0 = q0 * iz0;
+        const double usr = (q1r * zr + q1i * zi) * im1, usi = (q1i * zr - q1r * zi) * im1;
+        const double ut0 = l0 * iz0;
+        const double utr = (l1r * zr + l1i * zi) * im1, uti = (l1i * zr - l1r * zi) * im1;
+        const double u0 = fma(up, ut0, us0), ur = fma(up, utr, usr), ui = fma(up, uti, usi);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) psi[a] = cM.V0[a] * u0 + 2.0 * (cM.V1re[a] * ur - cM.V1im[a] * ui);
+        t_aff = cM.V0[2] * ut0 + 2.0 * (cM.V1re[2] * utr - cM.V1im[2] * uti);
+        s_aff = cM.V0[2] * us0 + 2.0 * (cM.V1re[2] * usr - cM.V1im[2] * usi);
+    }
+}
+
+template <int P, int LOG2GB>
+__global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) {
+    constexpr int NP1 = P + 1;
+    constexpr int GB = 1 << LOG2GB;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int gl = lane & (GB - 1), dl = lane >> LOG2GB;
+    const StreamDesc sd = prm.streams[blockIdx.x];
+    const bool fx = (sd.quadrant & 1) != 0;
+    const bool d_on = dl < sd.nd, g_on = gl < sd.ng;
+    const int g = sd.g0 + gl;
+    const int nx = prm.nx, G = prm.G;
+    extern __shared__ __align__(16) double sm1[];
+    double* TS = sm1;                       // [nseg][32][2]
+    double* IN = TS + prm.nseg * 64;        // [nseg][32]
+    double c = 0.0, cm0 = 0.0, cm1 = 0.0, cm2 = 0.0, bw0 = 0.0, bw1 = 0.0, jw0 = 0.0, jw1 = 0.0;
+    if (d_on && g_on) {
+        const DirConst& D = prm.dirs[sd.d0 + dl];
+        c = D.cx;
+        cm0 = D.mom[0];
+        cm1 = D.mom[1];
+        cm2 = D.mom[2];
+        bw0 = D.bw[0];
+        bw1 = D.bw[1];
+        jw0 = D.jw[0];
+        jw1 = D.jw[1];
+    }
+    const int e_begin = w * prm.seglen;
+    const int e_end = min(nx, e_begin + prm.seglen);
+    double* slab = prm.slabs + (size_t)blockIdx.x * prm.out_size;
+    const size_t nodes = prm.nodes;
+
+    auto load = [&](int ip, double& st, double (&q)[NP1]) {
+        const int i = fx ? nx - 1 - ip : ip;
+        st = 1.0;
+#pragma unroll
+        for (int a = 0; a < NP1; ++a) q[a] = 0.0;
+        if (g_on) {
+            st = prm.sigma[(size_t)i * G + g] + prm.inv_c_dt;
+            if (bad_sigma(st)) atomicOr(prm.err, 1);
+#pragma unroll
+            for (int aq = 0; aq < NP1; ++aq) {
+                const int a = fx ? P - aq : aq;
+                q[aq] = prm.q[((size_t)i * NP1 + a) * G + g];
+            }
+        }
+    };
+
+    // phase 1: compose the affine maps of this segment
+    double Tm = 1.0, Sm = 0.0;
+    for (int ip = e_begin; ip < e_end; ++ip) {
+        double st, q[NP1], psi[NP1], ta, sa;
+        load(ip, st, q);
+        solve1d<P>(c, st, q, 0.0, psi, ta, sa);
+        Sm = fma(ta, Sm, sa);
+        Tm = ta * Tm;
+    }
+    TS[(w * 32 + lane) * 2 + 0] = Tm;
+    TS[(w * 32 + lane) * 2 + 1] = Sm;
+    __syncthreads();
+    // phase 2: segment inflows, sequential over segments
+    if (w == 0) {
+        double psi_in = 0.0;
+        if (g_on) psi_in = prm.inflow[(size_t)(fx ? 1 : 0) * G + g];
+        for (int k = 0; k < prm.nseg; ++k) {
+            IN[k * 32 + lane] = psi_in;
+            psi_in = fma(TS[(k * 32 + lane) * 2 + 0], psi_in, TS[(k * 32 + lane) * 2 + 1]);
+        }
+    }
+    __syncthreads();
+    // phase 3: final sweep of the segment + moments
+    double up = IN[w * 32 + lane];
+    for (int ip = e_begin; ip < e_end; ++ip) {
+        double st, q[NP1], psi[NP1], ta, sa;
+        load(ip, st, q);
+        solve1d<P>(c, st, q, up, psi, ta, sa);
+        up = psi[P];
+        const int i = fx ? nx - 1 - ip : ip;
+        double v[3 * NP1];
+#pragma unroll
+        for (int aq = 0; aq < NP1; ++aq) {
+            v[0 * NP1 + aq] = cm0 * psi[aq];
+            v[1 * NP1 + aq] = cm1 * psi[aq];
+            v[2 * NP1 + aq] = cm2 * psi[aq];
+        }
+        auto sink = [&](int idx, double val) {
+            if (idx < 3 * NP1) {
+                const int m = idx / NP1, aq = idx - m * NP1;
+                const int a = fx ? P - aq : aq;
+                slab[(size_t)m * nodes + (size_t)i * NP1 + a] = val;
+            }
+        };
+        ReduceScatter<3 * NP1, 16>::run(v, lane, 0, 3 * NP1, sink);
+        if (i == 0 || i == nx - 1) {  // warp-uniform
+            // boundary closures at x = 0 (node a = 0) and x = lx (node a = P)
+            const double p0 = psi[fx ? P : 0], p1 = psi[fx ? 0 : P];
+            double bv[4];
+            bv[0] = (i == 0) ? bw0 * p0 : 0.0;
+            bv[1] = (i == nx - 1) ? bw1 * p1 : 0.0;
+            bv[2] = (i == 0) ? jw0 * p0 : 0.0;
+            bv[3] = (i == nx - 1) ? jw1 * p1 : 0.0;
+            auto bsink = [&](int idx, double val) {
+                if (idx < 4) {
+                    const int face = idx & 1, isj = idx >> 1;
+                    const bool mine = (face == 0) ? (i == 0) : (i == nx - 1);
+                    if (mine) slab[3 * nodes + 2 * isj + face] = val;
+                }
+            };
+            ReduceScatter<4, 16>::run(bv, lane, 0, 4, bsink);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ finalize
+__global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, size_t n, double* __restrict__ out,
+                                int* err) {
+    bool bad = false;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < n_slabs; ++s) acc += __ldcs(slabs + (size_t)s * n + i);
+        out[i] = acc;
+        bad |= !(fabs(acc) < 1.0e300);
+    }
+    if (bad) atomicOr(err, 2);
+}
+
+// ------------------------------------------------------------------ launchers
+template <int P>
+static const void* pick2d(int log2gb) {
+    switch (log2gb) {
+        case 0: return (const void*)sweep2d_kernel<P, 0>;
+        case 1: return (const void*)sweep2d_kernel<P, 1>;
+        case 2: return (const void*)sweep2d_kernel<P, 2>;
+        case 3: return (const void*)sweep2d_kernel<P, 3>;
+        case 4: return (const void*)sweep2d_kernel<P, 4>;
+        default: return (const void*)sweep2d_kernel<P, 5>;
+    }
+}
+template <int P>
+static const void* pick1d() {
+    return (const void*)sweep1d_kernel<P, 0>;
+}
+
+int upload_modal(const ModalConsts& mc) { return (int)cudaMemcpyToSymbol(cM, &mc, sizeof(ModalConsts)); }
+
+int sweep2d_smem_bytes(int p, int gb, int dset) {
+    const int T = rows_per_strip(p), C = cols_per_chunk(p), NQ = nq_of(p);
+    const int CT = C * T;
+    return (CT * NQ * gb + CT * gb + CT * dset * NQ) * (int)sizeof(double);
+}
+int sweep2d_rows_per_strip(int p) { return rows_per_strip(p); }
+int sweep2d_cols_per_chunk(int p) { return cols_per_chunk(p); }
+
+int sweep2d_occupancy(int p, int log2gb, int block, size_t smem, int* blocks_per_sm) {
+    const void* f = (p == 2) ? pick2d<2>(log2gb) : pick2d<1>(log2gb);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+}
+
+int launch_sweep2d(int p, int log2gb, const Sweep2DParams& prm, int grid, int block, size_t smem, void* stream) {
+    const void* f = (p == 2) ? pick2d<2>(log2gb) : pick2d<1>(log2gb);
+    void* args[] = {(void*)&prm};
+    return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
+}
+
+int launch_sweep1d(int p, int log2gb, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream) {
+    const void* f;
+    switch (p * 8 + log2gb) {
+        case 8 + 0: f = (const void*)sweep1d_kernel<1, 0>; break;
+        case 8 + 1: f = (const void*)sweep1d_kernel<1, 1>; break;
+        case 8 + 2: f = (const void*)sweep1d_kernel<1, 2>; break;
+        case 8 + 3: f = (const void*)sweep1d_kernel<1, 3>; break;
+        case 8 + 4: f = (const void*)sweep1d_kernel<1, 4>; break;
+        case 8 + 5: f = (const void*)sweep1d_kernel<1, 5>; break;
+        case 16 + 0: f = (const void*)sweep1d_kernel<2, 0>; break;
+        case 16 + 1: f = (const void*)sweep1d_kernel<2, 1>; break;
+        case 16 + 2: f = (const void*)sweep1d_kernel<2, 2>; break;
+        case 16 + 3: f = (const void*)sweep1d_kernel<2, 3>; break;
+        case 16 + 4: f = (const void*)sweep1d_kernel<2, 4>; break;
+        default: f = (const void*)sweep1d_kernel<2, 5>; break;
+    }
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+    }
+    void* args[] = {(void*)&prm};
+    return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
+}
+
+int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream) {
+    const int block = 256;
+    size_t want = (out_size + block - 1) / block;
+    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+    if (grid < 1) grid = 1;
+    finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, out_size, out, err);
+    return (int)cudaGetLastError();
+}
+
+const char* cuda_err_string(int e) { return cudaGetErrorString((cudaError_t)e); }
+
+// FP64 pipe probe: 8 independent DFMA chains per thread, enough warps per SM to
+// hide the DFMA latency.  flops = 2 * 8 * iters per thread.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters, double b, double c) {
+    double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+           a7 = a0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fma(a0, b, c);
+            a1 = fma(a1, b, c);
+            a2 = fma(a2, b, c);
+            a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c);
+            a5 = fma(a5, b, c);
+            a6 = fma(a6, b, c);
+            a7 = fma(a7, b, c);
+        }
+    }
+    const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == 1.2345) sink[threadIdx.x] = r;  // keep the chains alive
+}
+
+int fp64_probe(int device, double* tflops) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e) return (int)e;
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    double* sink = nullptr;
+    if ((e = cudaMalloc(&sink, 256 * sizeof(double)))) return (int)e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int iters = 4096, blocks = nsm * 8, threads = 256;
+    fp64_probe_kernel<<<blocks, threads>>>(sink, 64, 0.999999, 1e-7);  // warm up
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        fp64_probe_kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-7);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e) return (int)e;
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return 0;
+}
+
+}  // namespace sweepk

@@ -1,0 +1,240 @@
+"""Thin ctypes binding of libsweep.so (include/sweep.h).  Argument marshalling
+only: every step of the sweep runs in the library's CUDA kernels.  There is no
+CPU fallback — if the library or a CUDA device is missing, construction fails.
+
+PyTorch is used for device memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsweep.so")
+
+SWEEP_OK, E_ARG, E_QUAD, E_SIGMA, E_CUDA, E_NCCL, E_INTERNAL = range(7)
+FOLD_Z = 1
+DETERMINISTIC = 2
+_NAMES = {1: "E_ARG", 2: "E_QUAD", 3: "E_SIGMA", 4: "E_CUDA", 5: "E_NCCL", 6: "E_INTERNAL"}
+
+# every symbol include/sweep.h declares
+EXPORTS = ("sweep_setup", "sweep_layout", "sweep_run", "closures_get", "sweep_run_host",
+           "sweep_stats", "sweep_timing", "sweep_kernel_times", "sweep_fp64_probe",
+           "sweep_nccl_unique_id", "sweep_destroy", "sweep_last_error")
+
+
+class SweepError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class sweep_desc(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("nx", ctypes.c_int), ("ny", ctypes.c_int),
+                ("lx", ctypes.c_double), ("ly", ctypes.c_double), ("p", ctypes.c_int),
+                ("n_dir", ctypes.c_int), ("omega", ctypes.POINTER(ctypes.c_double)),
+                ("w", ctypes.POINTER(ctypes.c_double)), ("n_group_local", ctypes.c_int),
+                ("group_offset", ctypes.c_int), ("n_group_total", ctypes.c_int), ("device", ctypes.c_int),
+                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("flags", ctypes.c_uint)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libsweep.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built: run `python -m paper_2504_21784_b200.build` "
+                               "(or __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(path)
+        vp, sz, dp, i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int
+        lib.sweep_setup.argtypes = [ctypes.POINTER(sweep_desc), ctypes.POINTER(vp)]
+        lib.sweep_setup.restype = i
+        lib.sweep_layout.argtypes = [vp, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+        lib.sweep_layout.restype = i
+        lib.sweep_run.argtypes = [vp, dp, ctypes.c_double, dp, dp, vp]
+        lib.sweep_run.restype = i
+        lib.closures_get.argtypes = [vp, dp, sz, vp]
+        lib.closures_get.restype = i
+        lib.sweep_run_host.argtypes = [vp, dp, ctypes.c_double, dp, dp, dp, sz, vp]
+        lib.sweep_run_host.restype = i
+        lib.sweep_stats.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+        lib.sweep_stats.restype = i
+        lib.sweep_timing.argtypes = [vp, i]
+        lib.sweep_timing.restype = i
+        lib.sweep_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i, ctypes.POINTER(i)]
+        lib.sweep_kernel_times.restype = i
+        lib.sweep_fp64_probe.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
+        lib.sweep_fp64_probe.restype = i
+        lib.sweep_nccl_unique_id.argtypes = [vp]
+        lib.sweep_nccl_unique_id.restype = i
+        lib.sweep_destroy.argtypes = [vp]
+        lib.sweep_destroy.restype = None
+        lib.sweep_last_error.argtypes = [vp]
+        lib.sweep_last_error.restype = ctypes.c_char_p
+        _lib = lib
+    return _lib
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    rc = lib.sweep_nccl_unique_id(buf)
+    if rc:
+        raise SweepError(rc, lib.sweep_last_error(None).decode())
+    return buf.raw
+
+
+def fp64_probe(device: int = 0) -> float:
+    """Measured FP64 FMA throughput of the device in TFLOP/s."""
+    lib = load_library()
+    t = ctypes.c_double()
+    rc = lib.sweep_fp64_probe(device, ctypes.byref(t))
+    if rc:
+        raise SweepError(rc, lib.sweep_last_error(None).decode())
+    return t.value
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class Sweep:
+    """One sweep configuration (mesh, order, quadrature, group shard) on one GPU."""
+
+    def __init__(self, dim: int, nx: int, ny: int, p: int, omega, w, n_group_local: int,
+                 lx: float = 1.0, ly: float = 1.0, device: int = 0, fold_z: bool = True,
+                 nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 group_offset: int = 0, n_group_total: int | None = None):
+        self._lib = load_library()
+        self._om = np.ascontiguousarray(omega, dtype=np.float64).reshape(-1, 3)
+        self._w = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
+        d = sweep_desc()
+        d.dim, d.nx, d.ny, d.lx, d.ly, d.p = dim, nx, (ny if dim == 2 else 1), lx, ly, p
+        d.n_dir = self._om.shape[0]
+        d.omega, d.w = _dptr(self._om), _dptr(self._w)
+        d.n_group_local = n_group_local
+        d.group_offset = group_offset
+        d.n_group_total = n_group_total if n_group_total is not None else n_group_local
+        d.device, d.nranks, d.rank = device, nranks, rank
+        self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        d.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None
+        d.flags = FOLD_Z if fold_z else 0
+        h = ctypes.c_void_p()
+        rc = self._lib.sweep_setup(ctypes.byref(d), ctypes.byref(h))
+        if rc:
+            raise SweepError(rc, self._lib.sweep_last_error(None).decode())
+        self._h = h
+        self.dim, self.nx, self.ny, self.p, self.G = dim, nx, (ny if dim == 2 else 1), p, n_group_local
+        self.device = device
+        off = (ctypes.c_size_t * 5)()
+        tot = ctypes.c_size_t()
+        self._check(self._lib.sweep_layout(self._h, off, ctypes.byref(tot)))
+        self.offsets = list(off)
+        self.out_size = tot.value
+
+    # ---------------------------------------------------------------- helpers
+    def _check(self, rc: int):
+        if rc:
+            raise SweepError(rc, self._lib.sweep_last_error(self._h).decode())
+
+    @staticmethod
+    def _stream_ptr(stream) -> int | None:
+        if stream is None:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        return int(stream)
+
+    # ---------------------------------------------------------------- ABI calls
+    def sweep_run(self, sigma, inv_c_dt: float, q, inflow, stream=None) -> None:
+        """sigma [N_el][G], q [N_el][n][G], inflow [N_bnode][G]: contiguous float64 CUDA tensors."""
+        for t in (sigma, q, inflow):
+            if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
+                raise ValueError("inputs must be contiguous float64 CUDA tensors")
+        self._check(self._lib.sweep_run(self._h, sigma.data_ptr(), float(inv_c_dt), q.data_ptr(),
+                                        inflow.data_ptr(), self._stream_ptr(stream)))
+
+    def closures_get(self, out=None, stream=None):
+        """Packed gray output phi|J|T|beta|J+ into out (device or host tensor)."""
+        import torch
+        if out is None:
+            out = torch.empty(self.out_size, dtype=torch.float64, device=f"cuda:{self.device}")
+        if out.numel() != self.out_size or not out.is_contiguous():
+            raise ValueError("out must be contiguous with out_size elements")
+        self._check(self._lib.closures_get(self._h, out.data_ptr(), self.out_size, self._stream_ptr(stream)))
+        return out
+
+    def sweep_run_host(self, sigma: np.ndarray, inv_c_dt: float, q: np.ndarray, inflow: np.ndarray,
+                       out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        """End-to-end with host arrays (pinned numpy views of torch pinned tensors recommended)."""
+        if out is None:
+            out = np.empty(self.out_size)
+        self._check(self._lib.sweep_run_host(self._h, sigma.ctypes.data, float(inv_c_dt), q.ctypes.data,
+                                             inflow.ctypes.data, out.ctypes.data, self.out_size,
+                                             self._stream_ptr(stream)))
+        return out
+
+    def stats(self) -> dict:
+        a = (ctypes.c_longlong * 4)()
+        self._check(self._lib.sweep_stats(self._h, a))
+        return {"launches": a[0], "directions_swept": a[1], "streams": a[2], "ctas": a[3]}
+
+    def timing(self, enable: bool = True) -> None:
+        self._check(self._lib.sweep_timing(self._h, 1 if enable else 0))
+
+    def kernel_times(self, max_runs: int = 1024) -> np.ndarray:
+        """[runs][3] ms: sweep kernel, finalize kernel, all-reduce."""
+        buf = (ctypes.c_double * (3 * max_runs))()
+        n = ctypes.c_int()
+        self._check(self._lib.sweep_kernel_times(self._h, buf, max_runs, ctypes.byref(n)))
+        return np.array(buf[:3 * n.value]).reshape(n.value, 3)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sweep_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def unpack(self, out) -> dict:
+        """Named views of a packed output (numpy or torch)."""
+        n = (self.p + 1) ** self.dim
+        nel = self.nx * self.ny
+        o = self.offsets
+        nT = 1 if self.dim == 1 else 3
+        return {"phi": out[o[0]:o[1]].reshape(nel, n), "J": out[o[1]:o[2]].reshape(self.dim, nel, n),
+                "T": out[o[2]:o[3]].reshape(nT, nel, n), "beta": out[o[3]:o[4]], "Jplus": out[o[4]:]}
+
+
+def from_problem(prob, device: int = 0, fold_z: bool = True, **kw) -> Sweep:
+    """Sweep handle for a synth.Problem-like object (dim, nx, ny, p, omega, w, G, lx, ly)."""
+    return Sweep(prob.dim, prob.nx, prob.ny, prob.p, prob.omega, prob.w, prob.sigma.shape[1],
+                 lx=prob.lx, ly=prob.ly, device=device, fold_z=fold_z, **kw)
+
+
+def run_problem(prob, device: int = 0, fold_z: bool = True) -> np.ndarray:
+    """Convenience: copy a problem to the GPU, sweep once, return the packed output (numpy)."""
+    import torch
+    dev = torch.device(f"cuda:{device}")
+    with from_problem(prob, device, fold_z) as sw:
+        s = torch.from_numpy(np.ascontiguousarray(prob.sigma)).to(dev)
+        q = torch.from_numpy(np.ascontiguousarray(prob.q)).to(dev)
+        f = torch.from_numpy(np.ascontiguousarray(prob.inflow)).to(dev)
+        sw.sweep_run(s, prob.inv_c_dt, q, f)
+        out = sw.closures_get()
+        return out.cpu().numpy()

@@ -112,7 +112,7 @@ def _left_edge_inflow(dim: int, nx: int, ny: int, p: int, values_g: np.ndarray) 
 def _opaque_blocks(cfg: int, nx: int, ny: int, block: int = 8, frac: float = 0.3) -> np.ndarray:
     """Reading R13: exactly round(frac * N_blocks) 8x8 blocks by seeded permutation.
     Returns a bool mask [ny][nx] (True = opaque)."""
-    nbx, nby = max(nx // block, 1), max(ny // block, 1)
+    nbx, nby = -(-nx // block), -(-ny // block)
     nb = nbx * nby
     k = int(round(frac * nb))
     perm = rng_for(cfg, F_BLOCKS).permutation(nb)[:k]

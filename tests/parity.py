@@ -1,0 +1,50 @@
+"""Field-wise parity metric shared by the GPU tests and bench.py (comparison only,
+no method arithmetic)."""
+from __future__ import annotations
+
+import numpy as np
+
+TOL = 1e-11          # north_star: relative L-infinity error per output field, FP64
+TINY = 1e-8          # a field whose reference norm is below TINY * |phi| is compared absolutely
+ABS_TOL = 1e-13      # ... with |delta| <= ABS_TOL * |phi|
+
+
+def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
+    n = (p + 1) ** dim
+    nel = nx * (ny if dim == 2 else 1)
+    nodes = nel * n
+    nb = 2 if dim == 1 else 2 * (nx + ny) * (p + 1)
+    names = ["phi"] + [f"J{c}" for c in "xy"[:dim]] + (["Txx"] if dim == 1 else ["Txx", "Txy", "Tyy"])
+    f, o = {}, 0
+    for nm in names:
+        f[nm] = out[o:o + nodes]
+        o += nodes
+    f["beta"] = out[o:o + nb]
+    f["Jplus"] = out[o + nb:o + 2 * nb]
+    assert o + 2 * nb == out.size, (o + 2 * nb, out.size)
+    return f
+
+
+def field_errors(got: np.ndarray, ref: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
+    """{field: (error, kind)} with kind 'rel' (|d|/|ref|) or 'abs_phi' (|d|/|phi|)."""
+    fg, fr = fields(got, dim, nx, ny, p), fields(ref, dim, nx, ny, p)
+    phi = max(np.abs(fr["phi"]).max(), 1e-300)
+    res = {}
+    for k in fr:
+        d = np.abs(fg[k] - fr[k]).max() if fr[k].size else 0.0
+        if not np.isfinite(d):
+            res[k] = (np.inf, "rel")
+            continue
+        nref = np.abs(fr[k]).max() if fr[k].size else 0.0
+        if nref >= TINY * phi:
+            res[k] = (d / nref, "rel")
+        else:
+            res[k] = (d / phi, "abs_phi")
+    return res
+
+
+def assert_parity(got, ref, dim, nx, ny, p, tol=TOL):
+    errs = field_errors(got, ref, dim, nx, ny, p)
+    bad = {k: v for k, v in errs.items() if v[0] > (tol if v[1] == "rel" else ABS_TOL)}
+    assert not bad, f"parity failed: {bad} (all: {errs})"
+    return errs
