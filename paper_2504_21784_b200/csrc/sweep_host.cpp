@@ -92,7 +92,7 @@ struct sweep_handle {
     size_t nodes, out_size, off[5];
     int n_dir_in, n_dir_eff;
     // schedule
-    int log2gb, gb, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
+    int log2gb, gb, kpl, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
     size_t smem;
     // device workspace
     DirConst* d_dirs = nullptr;
@@ -402,17 +402,28 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     }
     qstart[nquad] = (int)table.size();
 
-    // lane layout: GB lanes per direction (consecutive groups), 32/GB directions per warp
+    // lane layout: GB lanes per direction (consecutive groups), 32/GB directions per
+    // warp; in 2-D each lane carries kpl groups, so a stream covers GB*kpl groups
     const int gbw = std::min(32, 1 << ilog2_ceil(h->G));
-    h->gb = gbw;
-    h->log2gb = ilog2_ceil(gbw);
-    const int n_gblocks = (h->G + gbw - 1) / gbw;
-    const int dirs_per_warp = 32 / gbw;
+    // 2-D p=2 with many groups: 4 groups per lane over 16 lanes (one CTA holds a
+    // whole quadrant's directions); otherwise 1 group per lane over up to 32 lanes
+    if (D.dim == 2 && D.p == 2 && h->G >= 64) {
+        h->kpl = 4;
+        h->gb = 16;
+        h->log2gb = 4;
+    } else {
+        h->kpl = 1;
+        h->gb = gbw;
+        h->log2gb = ilog2_ceil(gbw);
+    }
+    const int gbk = h->gb * h->kpl;
+    const int n_gblocks = (h->G + gbk - 1) / gbk;
+    const int dirs_per_warp = 32 / h->gb;
     int maxq = 1;
     for (int q = 0; q < nquad; ++q) maxq = std::max(maxq, (int)byq[q].size());
     std::vector<StreamDesc> streams;
     if (D.dim == 2) {
-        const int nw = std::min(16, std::max(1, (maxq + dirs_per_warp - 1) / dirs_per_warp));
+        const int nw = std::min(8, std::max(1, (maxq + dirs_per_warp - 1) / dirs_per_warp));
         h->block = 32 * nw;
         h->dset = nw * dirs_per_warp;
     } else {
@@ -420,12 +431,12 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     }
     for (int q = 0; q < nquad; ++q) {
         const int nq = (int)byq[q].size();
-        for (int gbk = 0; gbk < n_gblocks; ++gbk)
+        for (int gbi = 0; gbi < n_gblocks; ++gbi)
             for (int d0 = 0; d0 < nq; d0 += h->dset) {
                 StreamDesc s;
                 s.quadrant = q;
-                s.g0 = gbk * gbw;
-                s.ng = std::min(gbw, h->G - s.g0);
+                s.g0 = gbi * gbk;
+                s.ng = std::min(gbk, h->G - s.g0);
                 s.d0 = qstart[q] + d0;
                 s.nd = std::min(h->dset, nq - d0);
                 streams.push_back(s);
@@ -464,13 +475,13 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     // schedule + workspace
     cudaError_t ce;
     if (D.dim == 2) {
-        const int T = sweepk::sweep2d_rows_per_strip(h->p), C = sweepk::sweep2d_cols_per_chunk(h->p);
+        const int T = sweepk::sweep2d_rows_per_strip(h->p, h->kpl), C = sweepk::sweep2d_cols_per_chunk(h->p, h->kpl);
         h->n_strips = (h->ny + T - 1) / T;
         h->n_chunks = (h->nx + C - 1) / C;
         h->n_tasks = h->n_strips * h->n_streams;
-        h->smem = (size_t)sweepk::sweep2d_smem_bytes(h->p, gbw, h->dset);
+        h->smem = (size_t)sweepk::sweep2d_smem_bytes(h->p, h->kpl, gbk, h->dset);
         int bps = 0;
-        int oe = sweepk::sweep2d_occupancy(h->p, h->log2gb, h->block, h->smem, &bps);
+        int oe = sweepk::sweep2d_occupancy(h->p, h->log2gb, h->kpl, h->block, h->smem, &bps);
         if (oe || bps < 1) {
             if (oe) cuda_fail(h, (cudaError_t)oe, "occupancy");
             else h->err = "sweep2d kernel cannot be resident (registers/shared memory)";
@@ -481,7 +492,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->grid = std::min(h->n_tasks, bps * std::max(nsm, 1));
         const int NT = h->np1;
         h->progress_ints = (size_t)h->n_streams * h->n_strips;
-        if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * (size_t)h->n_streams * 2 * h->nx * NT * h->block)))
+        if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * (size_t)h->n_streams * 2 * (h->n_chunks * C) * h->kpl * NT * h->block)))
             return cuda_fail(h, ce, "cudaMalloc ytr"), bail(SWEEP_E_CUDA);
     } else {
         h->nseg = std::min(32, std::max(1, (h->nx + 15) / 16));
@@ -562,11 +573,14 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.nx = h->nx;
         prm.ny = h->ny;
         prm.G = h->G;
+        prm.nx_pad = h->n_chunks * sweepk::sweep2d_cols_per_chunk(h->p, h->kpl);
+        prm.bulk_ok = (h->G % 2 == 0) ? 1 : 0;
         prm.n_streams = h->n_streams;
         prm.n_strips = h->n_strips;
         prm.n_chunks = h->n_chunks;
         prm.n_tasks = h->n_tasks;
         prm.gb = h->gb;
+        prm.kpl = h->kpl;
         prm.dset = h->dset;
         prm.nbnode = h->nbnode;
         prm.inv_c_dt = inv_c_dt;
@@ -582,7 +596,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.out_size = h->out_size;
         prm.nodes = h->nodes;
         prm.err = h->d_err;
-        e = sweepk::launch_sweep2d(h->p, h->log2gb, prm, h->grid, h->block, h->smem, stream);
+        e = sweepk::launch_sweep2d(h->p, h->log2gb, h->kpl, prm, h->grid, h->block, h->smem, stream);
     } else {
         sweepk::Sweep1DParams prm;
         prm.nx = h->nx;

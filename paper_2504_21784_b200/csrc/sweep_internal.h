@@ -41,10 +41,13 @@ struct ModalConsts {
 
 struct Sweep2DParams {
     int nx, ny, G;                 // G = groups on this rank
+    int nx_pad;                    // n_chunks * C (trace ring row length)
     int n_streams, n_strips, n_chunks, n_tasks;
     int gb;                        // lanes per direction (power of 2)
+    int kpl;                       // groups per lane
     int dset;                      // directions per CTA
     int nbnode;
+    int bulk_ok;                   // q / sigma rows are 16-byte aligned (G even): 1-D bulk copies
     double inv_c_dt;
     const double* sigma;           // [N_el][G]
     const double* q;               // [N_el][n][G]
@@ -53,7 +56,7 @@ struct Sweep2DParams {
     const StreamDesc* streams;
     int* progress;                 // [n_streams][n_strips] chunks completed
     int* task_counter;
-    double* ytr;                   // [n_streams][2][nx][NT][NL]
+    double* ytr;                   // [n_streams][2][nx][K][NT][NL]
     double* slabs;                 // [n_streams][out_size]
     size_t out_size;
     size_t nodes;                  // N_el * n
@@ -76,13 +79,13 @@ struct Sweep1DParams {
 
 // launchers (sweep_kernels.cu); return cudaError_t as int
 int upload_modal(const ModalConsts& mc);
-int launch_sweep2d(int p, int log2gb, const Sweep2DParams& prm, int grid, int block, size_t smem, void* stream);
+int launch_sweep2d(int p, int log2lg, int k, const Sweep2DParams& prm, int grid, int block, size_t smem, void* stream);
 int launch_sweep1d(int p, int log2gb, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream);
 int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream);
-int sweep2d_smem_bytes(int p, int gb, int dset);
-int sweep2d_occupancy(int p, int log2gb, int block, size_t smem, int* blocks_per_sm);
-int sweep2d_rows_per_strip(int p);
-int sweep2d_cols_per_chunk(int p);
+int sweep2d_smem_bytes(int p, int k, int gbk, int dset);
+int sweep2d_occupancy(int p, int log2lg, int k, int block, size_t smem, int* blocks_per_sm);
+int sweep2d_rows_per_strip(int p, int k);
+int sweep2d_cols_per_chunk(int p, int k);
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
 

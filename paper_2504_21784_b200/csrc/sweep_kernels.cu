@@ -28,12 +28,26 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "sweep_internal.h"
 
 namespace sweepk {
 
 __constant__ ModalConsts cM;
+
+#ifdef SWEEP_TRACE
+// debug timeline (trace builds only): per task [start, end, waited ns, sm id]
+__device__ long long g_trace[1 << 18][4];
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+extern "C" int sweep_debug_trace(long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 4 * (size_t)n);
+}
+#endif
 
 #define FULLMASK 0xffffffffu
 
@@ -54,6 +68,17 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// 8-byte global->shared asynchronous copy; src_bytes = 0 zero-fills the slot.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int src_bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ bool bad_sigma(double st) { return !(st > 0.0) || !(st < 1.0e300); }
@@ -221,8 +246,11 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
     tyo[1] = u[3];
 }
 
-__host__ __device__ constexpr int rows_per_strip(int P) { return P == 2 ? 4 : 8; }
-__host__ __device__ constexpr int cols_per_chunk(int P) { return 8; }
+// Strip / chunk geometry as a function of (P, K): T element rows per strip,
+// C columns per chunk (one pipeline step).  K >= 4 lanes carry many groups, so
+// fewer rows keep the x-traces in registers.
+__host__ __device__ constexpr int rows_per_strip(int P, int K) { return K >= 4 ? 2 : (P == 2 ? 4 : 8); }
+__host__ __device__ constexpr int cols_per_chunk(int P, int K) { return K >= 4 ? 8 : 4; }
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
 
 __device__ __forceinline__ int bnode2d(int face, int idx, int node, int nx, int ny, int np1) {
@@ -234,33 +262,81 @@ __device__ __forceinline__ int bnode2d(int face, int idx, int node, int nx, int 
     }
 }
 
-template <int P, int LOG2GB>
-__global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm) {
+// ---- mbarrier + 1-D bulk copy (TMA engine) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Lane layout: LG = 2^LOG2LG consecutive lanes share one direction and hold
+// consecutive groups; each lane carries K groups (g, g + LG, ...), so a stream
+// (CTA) covers GBK = LG*K groups of NL/LG directions.  The K independent solves
+// per element give ILP and amortise the cross-lane group reduction.
+//
+// Per chunk (C columns x T rows of one strip):
+//   A  the raw q / sigma rows of chunk c+1 are fetched by 1-D bulk copies (TMA
+//      engine, mbarrier completion) into the other half of a double buffer while
+//      chunk c is swept; chunk c is then turned in place into sweep-ordered
+//      modal q^ (p=2) and sigma~ = sigma + 1/(c dt);
+//   B  every lane sweeps the chunk (branch-free: out-of-mesh rows/columns run on
+//      zeroed staging and are never written out);
+//   C  direction sums with the moment / boundary weights, back to nodal values,
+//      written to this stream's slab.
+template <int P, int LOG2LG, int K>
+__global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sweep2DParams prm) {
     constexpr int NP1 = P + 1;
     constexpr int NN = NP1 * NP1;
     constexpr int NQ = nq_of(P);
     constexpr int NT = NP1;  // trace reals per face (p=2: modal 1 real + 1 complex)
-    constexpr int GB = 1 << LOG2GB;
-    constexpr int T = rows_per_strip(P);
-    constexpr int C = cols_per_chunk(P);
+    constexpr int LG = 1 << LOG2LG;
+    constexpr int GBK = LG * K;
+    constexpr int T = rows_per_strip(P, K);
+    constexpr int C = cols_per_chunk(P, K);
     constexpr int CT = C * T;
     constexpr int NFIELD = 14;  // 6 moments + (beta, J+) x 4 faces
 
     const int NL = blockDim.x;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int gl = tid & (GB - 1);
-    const int dl = tid >> LOG2GB;
-    const int dset = NL >> LOG2GB;
+    const int gl = tid & (LG - 1);
+    const int dl = tid >> LOG2LG;
+    const int dset = NL >> LOG2LG;
 
-    extern __shared__ __align__(16) double smem[];
-    double* qs = smem;                 // [CT][NQ][GB]
-    double* ss = qs + CT * NQ * GB;    // [CT][GB]
-    double* S = ss + CT * GB;          // [CT][dset][NQ]
+    extern __shared__ __align__(128) double smem[];
+    double* qsb = smem;                      // [2][CT][NN][GBK]  (double buffer; modal in place for p=2)
+    double* ssb = qsb + 2 * CT * NN * GBK;   // [2][CT][GBK]
+    double* S = ssb + 2 * CT * GBK;          // [CT][dset][NQ]
+    __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ int s_task;
 
     const int nx = prm.nx, ny = prm.ny, G = prm.G;
     const size_t nodes = prm.nodes;
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_proxy_async();
+    }
+    unsigned phase_bits = 0;  // parity of the next completion of mbar[0] (bit 0) and mbar[1] (bit 1)
 
     for (;;) {
         if (tid == 0) s_task = atomicAdd(prm.task_counter, 1);
@@ -270,11 +346,13 @@ __global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm
         if (task >= prm.n_tasks) break;
         const int J = task / prm.n_streams;
         const int s = task - J * prm.n_streams;
+#ifdef SWEEP_TRACE
+        long long t_task0 = 0, t_waited = 0;
+        if (tid == 0) t_task0 = gtimer();
+#endif
         const StreamDesc sd = prm.streams[s];
         const bool fx = (sd.quadrant & 1) != 0, fy = (sd.quadrant & 2) != 0;
         const bool d_on = dl < sd.nd;
-        const bool g_on = gl < sd.ng;
-        const int g = sd.g0 + gl;
         double cx = 0.0, cy = 0.0;
         if (d_on) {
             cx = prm.dirs[sd.d0 + dl].cx;
@@ -283,78 +361,152 @@ __global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm
         const int j0 = J * T;
         const int rows = min(T, ny - j0);
         double* slab = prm.slabs + (size_t)s * prm.out_size;
+        const bool bulk = prm.bulk_ok && ((sd.ng & 1) == 0) && ((sd.g0 & 1) == 0);
+
+        // fetch chunk cc's raw q / sigma rows (physical node order) into buffer b
+        auto stage = [&](int cc, int b) {
+            double* qd = qsb + (size_t)b * CT * NN * GBK;
+            double* sdst = ssb + (size_t)b * CT * GBK;
+            const int i0s = cc * C;
+            const int colss = min(C, nx - i0s);
+            const int nel = colss * rows;
+            if (bulk) {
+                // warp 0 issues one copy per (element, node) row and one per sigma row
+                if (tid < 32) {
+                    const unsigned row_bytes = (unsigned)sd.ng * 8u;
+                    if (tid == 0) mbar_arrive_expect_tx(&mbar[b], row_bytes * (unsigned)(nel * (NN + 1)));
+                    __syncwarp();
+                    for (int it = tid; it < nel * (NN + 1); it += 32) {
+                        const int el0 = it / (NN + 1), kk = it - el0 * (NN + 1);
+                        const int col = el0 / rows, r = el0 - col * rows;
+                        const int el = col * T + r;
+                        const int ip = i0s + col, jp = j0 + r;
+                        const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                        const size_t e = (size_t)i + (size_t)nx * j;
+                        if (kk < NN)
+                            bulk_g2s(qd + ((size_t)el * NN + kk) * GBK, prm.q + (e * NN + kk) * G + sd.g0, row_bytes,
+                                     &mbar[b]);
+                        else
+                            bulk_g2s(sdst + (size_t)el * GBK, prm.sigma + e * G + sd.g0, row_bytes, &mbar[b]);
+                    }
+                }
+            } else {
+                for (int it = tid; it < CT * (NN + 1) * GBK; it += NL) {
+                    const int gg = it % GBK;
+                    const int rest = it / GBK;
+                    const int kk = rest % (NN + 1);
+                    const int el = rest / (NN + 1);
+                    const int col = el / T, r = el - col * T;
+                    if (col < colss && r < rows && gg < sd.ng) {
+                        const int ip = i0s + col, jp = j0 + r;
+                        const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                        const size_t e = (size_t)i + (size_t)nx * j;
+                        if (kk < NN)
+                            cp_async8(qd + ((size_t)el * NN + kk) * GBK + gg, prm.q + (e * NN + kk) * G + sd.g0 + gg, 8);
+                        else
+                            cp_async8(sdst + (size_t)el * GBK + gg, prm.sigma + e * G + sd.g0 + gg, 8);
+                    }
+                }
+                cp_async_commit();
+            }
+        };
+        auto wait_stage = [&](int b) {
+            if (bulk) {
+                mbar_wait(&mbar[b], (phase_bits >> b) & 1u);
+                phase_bits ^= 1u << b;
+            } else {
+                cp_async_wait<0>();
+            }
+        };
+        stage(0, 0);
 
         // x-inflow traces of the strip (domain boundary at i' = 0)
-        double tx[T][NT];
+        double tx[K][T][NT];
 #pragma unroll
-        for (int r = 0; r < T; ++r) {
-            double t[NP1];
+        for (int k = 0; k < K; ++k) {
+            const bool g_on = gl + k * LG < sd.ng;
+            const int g = sd.g0 + gl + k * LG;
 #pragma unroll
-            for (int bq = 0; bq < NP1; ++bq) t[bq] = 0.0;
-            if (r < rows && g_on) {
-                const int jp = j0 + r;
-                const int j = fy ? ny - 1 - jp : jp;
+            for (int r = 0; r < T; ++r) {
+                double t[NP1];
 #pragma unroll
-                for (int bq = 0; bq < NP1; ++bq) {
-                    const int b = fy ? P - bq : bq;
-                    t[bq] = prm.inflow[(size_t)bnode2d(fx ? 1 : 0, j, b, nx, ny, NP1) * G + g];
+                for (int bq = 0; bq < NP1; ++bq) t[bq] = 0.0;
+                if (r < rows && g_on) {
+                    const int jp = j0 + r;
+                    const int j = fy ? ny - 1 - jp : jp;
+#pragma unroll
+                    for (int bq = 0; bq < NP1; ++bq) {
+                        const int b = fy ? P - bq : bq;
+                        t[bq] = prm.inflow[(size_t)bnode2d(fx ? 1 : 0, j, b, nx, ny, NP1) * G + g];
+                    }
                 }
-            }
-            if constexpr (P == 2) {
-                tx[r][0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
-                tx[r][1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
-                tx[r][2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
-            } else {
-                tx[r][0] = t[0];
-                tx[r][1] = t[1];
+                if constexpr (P == 2) {
+                    tx[k][r][0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
+                    tx[k][r][1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
+                    tx[k][r][2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
+                } else {
+                    tx[k][r][0] = t[0];
+                    tx[k][r][1] = t[1];
+                }
             }
         }
 
         for (int c = 0; c < prm.n_chunks; ++c) {
             const int i0 = c * C;
             const int cols = min(C, nx - i0);
-            // ---- phase A: stage sigma~ and q (p=2: transformed to modal) for the chunk
-            for (int it = tid; it < CT * GB; it += NL) {
-                const int el = it >> LOG2GB;
-                const int gg = it & (GB - 1);
+            const int buf = c & 1;
+            double* qs = qsb + (size_t)buf * CT * NN * GBK;
+            double* ss = ssb + (size_t)buf * CT * GBK;
+            // ---- phase A: prefetch the next chunk, then finish this chunk's staging in place
+            if (c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);
+            wait_stage(buf);
+            if (!bulk && c + 1 < prm.n_chunks) {
+                // (cp.async path) the next chunk's group was committed after this one
+            }
+            __syncthreads();
+            for (int it = tid; it < CT * GBK; it += NL) {
+                const int el = it / GBK;
+                const int gg = it - el * GBK;
                 const int col = el / T, r = el - col * T;
+                const bool on = col < cols && r < rows && gg < sd.ng;
                 double st = 1.0;
                 double qv[NN];
 #pragma unroll
-                for (int k = 0; k < NN; ++k) qv[k] = 0.0;
-                if (col < cols && r < rows && gg < sd.ng) {
-                    const int ip = i0 + col, jp = j0 + r;
-                    const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                    const size_t e = (size_t)i + (size_t)nx * j;
-                    const int gq = sd.g0 + gg;
-                    st = prm.sigma[e * G + gq] + prm.inv_c_dt;
-                    if (bad_sigma(st)) atomicOr(prm.err, 1);
-#pragma unroll
-                    for (int k = 0; k < NN; ++k) {
-                        const int aq = k % NP1, bq = k / NP1;
-                        const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
-                        qv[k] = prm.q[(e * NN + a + NP1 * b) * G + gq];
-                    }
+                for (int kk = 0; kk < NN; ++kk) {
+                    const int aq = kk % NP1, bq = kk / NP1;
+                    const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
+                    qv[kk] = on ? qs[((size_t)el * NN + a + NP1 * b) * GBK + gg] : 0.0;
                 }
-                ss[el * GB + gg] = st;
+                if (on) {
+                    st = ss[el * GBK + gg] + prm.inv_c_dt;
+                    if (bad_sigma(st)) atomicOr(prm.err, 1);
+                }
+                ss[el * GBK + gg] = st;
                 if constexpr (P == 2) {
 #pragma unroll
                     for (int m = 0; m < 9; ++m) {
                         double acc = 0.0;
 #pragma unroll
-                        for (int k = 0; k < 9; ++k) acc = fma(cM.fwd[m][k], qv[k], acc);
-                        qs[(el * NQ + m) * GB + gg] = acc;
+                        for (int kk = 0; kk < 9; ++kk) acc = fma(cM.fwd[m][kk], qv[kk], acc);
+                        qs[((size_t)el * NN + m) * GBK + gg] = acc;
                     }
                 } else {
 #pragma unroll
-                    for (int k = 0; k < NN; ++k) qs[(el * NQ + k) * GB + gg] = qv[k];
+                    for (int kk = 0; kk < NN; ++kk) qs[((size_t)el * NN + kk) * GBK + gg] = qv[kk];
                 }
             }
             // ---- wait until the strip below has finished this chunk
+#ifndef SWEEP_ABL_NOWAIT
             if (J > 0 && tid == 0) {
+#else
+            if (false) {
+#endif
                 const int* f = prm.progress + (size_t)s * prm.n_strips + (J - 1);
                 // watchdog: a predecessor that never arrives (a bug) must not hang the GPU
                 const long long t_start = clock64();
+#ifdef SWEEP_TRACE
+                const long long w0 = gtimer();
+#endif
                 while (ld_acquire(f) < c + 1) {
                     __nanosleep(32);
                     if (clock64() - t_start > (1LL << 34)) {
@@ -362,107 +514,92 @@ __global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm
                         break;
                     }
                 }
+#ifdef SWEEP_TRACE
+                t_waited += gtimer() - w0;
+#endif
             }
             __syncthreads();
 
-            // ---- phase B: sweep the chunk, column by column, rows bottom to top
-            if constexpr (P == 2) {
-                const LaneP2 L = make_lane_p2(cx, cy);
-                for (int col = 0; col < cols; ++col) {
-                    const int ip = i0 + col;
-                    double ty[NT];
-                    if (J == 0) {
-                        double t[NP1] = {0.0, 0.0, 0.0};
-                        if (g_on) {
-                            const int i = fx ? nx - 1 - ip : ip;
+            // ---- phase B: sweep the chunk, column by column, rows bottom to top (branch-free)
+            using LaneC = typename std::conditional<P == 2, LaneP2, LaneP1>::type;
+            LaneC L;
+            if constexpr (P == 2) L = make_lane_p2(cx, cy);
+            else L = make_lane_p1(cx, cy);
+            const int nxp = prm.nx_pad;
+            const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)(K * NT) * NL;
+            double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)(K * NT) * NL;
+            const bool write_y = J + 1 < prm.n_strips;
+#pragma unroll 1
+            for (int col = 0; col < C; ++col) {
+                const int ip = i0 + col;
+                double ty[K][NT];
+                if (J == 0) {
+                    const bool col_on = ip < nx;
+                    const int i = fx ? nx - 1 - ip : ip;
 #pragma unroll
-                            for (int aq = 0; aq < NP1; ++aq) {
-                                const int a = fx ? P - aq : aq;
-                                t[aq] = prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g];
-                            }
+                    for (int k = 0; k < K; ++k) {
+                        const bool on = col_on && (gl + k * LG < sd.ng);
+                        const int g = sd.g0 + gl + k * LG;
+                        double t[NP1];
+#pragma unroll
+                        for (int aq = 0; aq < NP1; ++aq) {
+                            const int a = fx ? P - aq : aq;
+                            t[aq] = on ? prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g] : 0.0;
                         }
-                        ty[0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
-                        ty[1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
-                        ty[2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
-                    } else {
-                        const double* src = prm.ytr + (((size_t)s * 2 + ((J - 1) & 1)) * nx + ip) * NT * NL;
-#pragma unroll
-                        for (int t = 0; t < NT; ++t) ty[t] = __ldcg(src + t * NL + tid);
-                    }
-#pragma unroll
-                    for (int r = 0; r < T; ++r) {
-                        if (r < rows) {
-                            const int el = col * T + r;
-                            double qh[9], u[9], txo[3], tyo[3];
-#pragma unroll
-                            for (int m = 0; m < 9; ++m) qh[m] = qs[(el * NQ + m) * GB + gl];
-                            const double st = ss[el * GB + gl];
-                            solve_p2(L, st, qh, tx[r], ty, u, txo, tyo);
-#pragma unroll
-                            for (int t = 0; t < 3; ++t) {
-                                tx[r][t] = txo[t];
-                                ty[t] = tyo[t];
-                            }
-                            double* Sd = S + ((size_t)el * dset + dl) * NQ;
-                            auto sink = [&](int idx, double val) {
-                                if (idx < NQ) Sd[idx] = val;
-                            };
-                            ReduceScatter<9, GB / 2>::run(u, lane, 0, 9, sink);
+                        if constexpr (P == 2) {
+                            ty[k][0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
+                            ty[k][1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
+                            ty[k][2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
+                        } else {
+                            ty[k][0] = t[0];
+                            ty[k][1] = t[1];
                         }
                     }
-                    if (J + 1 < prm.n_strips) {
-                        double* dst = prm.ytr + (((size_t)s * 2 + (J & 1)) * nx + ip) * NT * NL;
+                } else {
 #pragma unroll
-                        for (int t = 0; t < NT; ++t) __stcg(dst + t * NL + tid, ty[t]);
-                    }
+                    for (int k = 0; k < K; ++k)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            ty[k][t] = __ldcg(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid);
                 }
-            } else {
-                const LaneP1 L = make_lane_p1(cx, cy);
-                for (int col = 0; col < cols; ++col) {
-                    const int ip = i0 + col;
-                    double ty[NT];
-                    if (J == 0) {
-                        ty[0] = ty[1] = 0.0;
-                        if (g_on) {
-                            const int i = fx ? nx - 1 - ip : ip;
 #pragma unroll
-                            for (int aq = 0; aq < NP1; ++aq) {
-                                const int a = fx ? P - aq : aq;
-                                ty[aq] = prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g];
-                            }
+                for (int r = 0; r < T; ++r) {
+                    const int el = col * T + r;
+                    double us[NQ];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        double qh[NQ], u[NQ], txo[NT], tyo[NT];
+#pragma unroll
+                        for (int m = 0; m < NQ; ++m) qh[m] = qs[((size_t)el * NN + m) * GBK + gl + k * LG];
+                        const double st = ss[el * GBK + gl + k * LG];
+                        if constexpr (P == 2) solve_p2(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
+                        else solve_p1(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            tx[k][r][t] = txo[t];
+                            ty[k][t] = tyo[t];
                         }
-                    } else {
-                        const double* src = prm.ytr + (((size_t)s * 2 + ((J - 1) & 1)) * nx + ip) * NT * NL;
 #pragma unroll
-                        for (int t = 0; t < NT; ++t) ty[t] = __ldcg(src + t * NL + tid);
+                        for (int m = 0; m < NQ; ++m) us[m] = (k == 0) ? u[m] : us[m] + u[m];
                     }
+                    double* Sd = S + ((size_t)el * dset + dl) * NQ;
+                    auto sink = [&](int idx, double val) { Sd[idx] = val; };
+#ifndef SWEEP_ABL_NORED
+                    ReduceScatter<NQ, LG / 2>::run(us, lane, 0, NQ, sink);
+#else
+                    if (lane == 0) Sd[0] = us[0] + us[1] + us[2] + us[3] + us[NQ - 1];
+#endif
+                }
+                if (write_y) {
 #pragma unroll
-                    for (int r = 0; r < T; ++r) {
-                        if (r < rows) {
-                            const int el = col * T + r;
-                            double qn[4], u[4], txo[2], tyo[2];
+                    for (int k = 0; k < K; ++k)
 #pragma unroll
-                            for (int m = 0; m < 4; ++m) qn[m] = qs[(el * NQ + m) * GB + gl];
-                            const double st = ss[el * GB + gl];
-                            solve_p1(L, st, qn, tx[r], ty, u, txo, tyo);
-                            tx[r][0] = txo[0];
-                            tx[r][1] = txo[1];
-                            ty[0] = tyo[0];
-                            ty[1] = tyo[1];
-                            double* Sd = S + ((size_t)el * dset + dl) * NQ;
-                            auto sink = [&](int idx, double val) {
-                                if (idx < NQ) Sd[idx] = val;
-                            };
-                            ReduceScatter<4, GB / 2>::run(u, lane, 0, 4, sink);
-                        }
-                    }
-                    if (J + 1 < prm.n_strips) {
-                        double* dst = prm.ytr + (((size_t)s * 2 + (J & 1)) * nx + ip) * NT * NL;
-#pragma unroll
-                        for (int t = 0; t < NT; ++t) __stcg(dst + t * NL + tid, ty[t]);
-                    }
+                        for (int t = 0; t < NT; ++t)
+                            __stcg(ydst + ((size_t)ip * K + k) * NT * NL + t * NL + tid, ty[k][t]);
                 }
             }
+            // this buffer is refilled by the async proxy two chunks from now
+            fence_proxy_async();
             __syncthreads();
             if (tid == 0) {
                 __threadfence();
@@ -471,6 +608,9 @@ __global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm
 
             // ---- phase C: sum over the CTA's directions with the moment / boundary
             // weights, back to nodal values, write this stream's slab
+#ifdef SWEEP_ABL_NOPHASEC
+            if (false)
+#endif
             for (int it = tid; it < CT * NFIELD; it += NL) {
                 const int el = it / NFIELD, f = it - el * NFIELD;
                 const int col = el / T, r = el - col * T;
@@ -496,24 +636,24 @@ __global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm
                 double psi[NN];
                 if constexpr (P == 2) {
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) {
+                    for (int kk = 0; kk < 9; ++kk) {
                         double acc = 0.0;
 #pragma unroll
-                        for (int m = 0; m < 9; ++m) acc = fma(cM.bck[k][m], M[m], acc);
-                        psi[k] = acc;
+                        for (int m = 0; m < 9; ++m) acc = fma(cM.bck[kk][m], M[m], acc);
+                        psi[kk] = acc;
                     }
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) psi[k] = M[k];
+                    for (int kk = 0; kk < 4; ++kk) psi[kk] = M[kk];
                 }
                 const size_t e = (size_t)i + (size_t)nx * j;
                 if (f < 6) {
                     double* dst = slab + (size_t)f * nodes + e * NN;
 #pragma unroll
-                    for (int k = 0; k < NN; ++k) {
-                        const int aq = k % NP1, bq = k / NP1;
+                    for (int kk = 0; kk < NN; ++kk) {
+                        const int aq = kk % NP1, bq = kk / NP1;
                         const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
-                        dst[a + NP1 * b] = psi[k];
+                        dst[a + NP1 * b] = psi[kk];
                     }
                 } else {
                     double* dst = slab + 6 * nodes + (((f - 6) & 1) ? prm.nbnode : 0);
@@ -535,6 +675,16 @@ __global__ void __launch_bounds__(512, 1) sweep2d_kernel(const Sweep2DParams prm
                 }
             }
         }
+#ifdef SWEEP_TRACE
+        if (tid == 0 && task < (1 << 18)) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_trace[task][0] = t_task0;
+            g_trace[task][1] = gtimer();
+            g_trace[task][2] = t_waited;
+            g_trace[task][3] = smid;
+        }
+#endif
     }
 }
 
@@ -706,16 +856,20 @@ __global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, s
 }
 
 // ------------------------------------------------------------------ launchers
-template <int P>
-static const void* pick2d(int log2gb) {
-    switch (log2gb) {
-        case 0: return (const void*)sweep2d_kernel<P, 0>;
-        case 1: return (const void*)sweep2d_kernel<P, 1>;
-        case 2: return (const void*)sweep2d_kernel<P, 2>;
-        case 3: return (const void*)sweep2d_kernel<P, 3>;
-        case 4: return (const void*)sweep2d_kernel<P, 4>;
-        default: return (const void*)sweep2d_kernel<P, 5>;
+template <int P, int K>
+static const void* pick2d_k(int log2lg) {
+    switch (log2lg) {
+        case 0: return (const void*)sweep2d_kernel<P, 0, K>;
+        case 1: return (const void*)sweep2d_kernel<P, 1, K>;
+        case 2: return (const void*)sweep2d_kernel<P, 2, K>;
+        case 3: return (const void*)sweep2d_kernel<P, 3, K>;
+        case 4: return (const void*)sweep2d_kernel<P, 4, K>;
+        default: return (const void*)sweep2d_kernel<P, 5, K>;
     }
+}
+static const void* pick2d(int p, int log2lg, int k) {
+    if (p == 2) return (k == 4) ? pick2d_k<2, 4>(log2lg) : pick2d_k<2, 1>(log2lg);
+    return (k == 4) ? pick2d_k<1, 4>(log2lg) : pick2d_k<1, 1>(log2lg);
 }
 template <int P>
 static const void* pick1d() {
@@ -724,23 +878,24 @@ static const void* pick1d() {
 
 int upload_modal(const ModalConsts& mc) { return (int)cudaMemcpyToSymbol(cM, &mc, sizeof(ModalConsts)); }
 
-int sweep2d_smem_bytes(int p, int gb, int dset) {
-    const int T = rows_per_strip(p), C = cols_per_chunk(p), NQ = nq_of(p);
+int sweep2d_smem_bytes(int p, int k, int gbk, int dset) {
+    const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k), NQ = nq_of(p), NN = (p + 1) * (p + 1);
     const int CT = C * T;
-    return (CT * NQ * gb + CT * gb + CT * dset * NQ) * (int)sizeof(double);
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * dset * NQ) * (int)sizeof(double);
 }
-int sweep2d_rows_per_strip(int p) { return rows_per_strip(p); }
-int sweep2d_cols_per_chunk(int p) { return cols_per_chunk(p); }
+int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
+int sweep2d_cols_per_chunk(int p, int k) { return cols_per_chunk(p, k); }
 
-int sweep2d_occupancy(int p, int log2gb, int block, size_t smem, int* blocks_per_sm) {
-    const void* f = (p == 2) ? pick2d<2>(log2gb) : pick2d<1>(log2gb);
+int sweep2d_occupancy(int p, int log2lg, int k, int block, size_t smem, int* blocks_per_sm) {
+    const void* f = pick2d(p, log2lg, k);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
 }
 
-int launch_sweep2d(int p, int log2gb, const Sweep2DParams& prm, int grid, int block, size_t smem, void* stream) {
-    const void* f = (p == 2) ? pick2d<2>(log2gb) : pick2d<1>(log2gb);
+int launch_sweep2d(int p, int log2lg, int k, const Sweep2DParams& prm, int grid, int block, size_t smem,
+                   void* stream) {
+    const void* f = pick2d(p, log2lg, k);
     void* args[] = {(void*)&prm};
     return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
 }

@@ -1,0 +1,48 @@
+"""Timeline of the persistent 2-D sweep: per task start/end/wait (trace build).
+usage: python profiles/trace_tasks.py [cfg]"""
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2504_21784_b200 import build as B  # noqa: E402
+import paper_2504_21784_b200.sweep as S  # noqa: E402
+import synth  # noqa: E402
+import torch  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+so = "/tmp/libsweep_trace.so"
+subprocess.check_call([B.nvcc(), *B.NVCC_FLAGS, "-DSWEEP_TRACE", "-I", os.path.join(ROOT, "include"), "-o", so,
+                       *B.SOURCES])
+S._lib = None
+lib = S.load_library(so)
+prob = synth.config(cfg)
+dev = torch.device("cuda:0")
+sig, q, fl = (torch.from_numpy(a).to(dev) for a in (prob.sigma, prob.q, prob.inflow))
+sw = S.from_problem(prob)
+for _ in range(3):
+    sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+torch.cuda.synchronize()
+st = sw.stats()
+sw.timing(True)
+sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+kt = sw.kernel_times(1)
+ntask = 4096
+buf = (ctypes.c_longlong * (4 * ntask))()
+lib.sweep_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+lib.sweep_debug_trace(buf, ntask)
+a = np.array(buf).reshape(-1, 4)
+a = a[a[:, 1] > 0]
+t0 = a[:, 0].min()
+start, end, wait = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, a[:, 2] / 1e3
+dur = end - start
+print(f"kernel {kt[0, 0]:.3f} ms; tasks {len(a)}; streams {st['streams']}; ctas {st['ctas']}")
+print(f"task duration us: mean {dur.mean():.1f} min {dur.min():.1f} max {dur.max():.1f}")
+print(f"wait us per task: mean {wait.mean():.1f} max {wait.max():.1f}; total wait fraction {wait.sum() / dur.sum():.3f}")
+print(f"last end {end.max():.1f} us; sum(dur)/ctas {dur.sum() / st['ctas']:.1f} us")
+for k in range(0, len(a), max(1, len(a) // 24)):
+    print(f"  task {k:5d} sm {a[k, 3]:3d} start {start[k]:9.1f} end {end[k]:9.1f} wait {wait[k]:8.1f}")
