@@ -371,12 +371,13 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             const int colss = min(C, nx - i0s);
             const int nel = colss * rows;
             if (bulk) {
-                // warp 0 issues one copy per (element, node) row and one per sigma row
-                if (tid < 32) {
+                // one copy per (element, node) row and one per sigma row, spread over
+                // all threads; thread 0 posts the byte count (the mbarrier tx-count may
+                // run negative until it does, the phase cannot complete before)
+                {
                     const unsigned row_bytes = (unsigned)sd.ng * 8u;
                     if (tid == 0) mbar_arrive_expect_tx(&mbar[b], row_bytes * (unsigned)(nel * (NN + 1)));
-                    __syncwarp();
-                    for (int it = tid; it < nel * (NN + 1); it += 32) {
+                    for (int it = tid; it < nel * (NN + 1); it += NL) {
                         const int el0 = it / (NN + 1), kk = it - el0 * (NN + 1);
                         const int col = el0 / rows, r = el0 - col * rows;
                         const int el = col * T + r;
@@ -419,6 +420,17 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             }
         };
         stage(0, 0);
+        // phase-C weights of this stream's directions: [dd][14]
+        double* coefS = S + (size_t)CT * dset * NQ;
+        for (int it = tid; it < dset * NFIELD; it += NL) {
+            const int dd = it / NFIELD, f = it - dd * NFIELD;
+            double v = 0.0;
+            if (dd < sd.nd) {
+                const DirConst* D = prm.dirs + sd.d0 + dd;
+                v = (f < 6) ? D->mom[f] : (((f - 6) & 1) ? D->jw[(f - 6) >> 1] : D->bw[(f - 6) >> 1]);
+            }
+            coefS[it] = v;
+        }
 
         // x-inflow traces of the strip (domain boundary at i' = 0)
         double tx[K][T][NT];
@@ -457,13 +469,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             const int buf = c & 1;
             double* qs = qsb + (size_t)buf * CT * NN * GBK;
             double* ss = ssb + (size_t)buf * CT * GBK;
-            // ---- phase A: prefetch the next chunk, then finish this chunk's staging in place
-            if (c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);
+            // ---- phase A: finish this chunk's staging in place (the copies were issued
+            // one chunk ago; bulk copies complete on the mbarrier each thread waits on)
+            if (!bulk && c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);
             wait_stage(buf);
-            if (!bulk && c + 1 < prm.n_chunks) {
-                // (cp.async path) the next chunk's group was committed after this one
-            }
-            __syncthreads();
+            if (!bulk) __syncthreads();
             for (int it = tid; it < CT * GBK; it += NL) {
                 const int el = it / GBK;
                 const int gg = it - el * GBK;
@@ -521,6 +531,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             __syncthreads();
 
             // ---- phase B: sweep the chunk, column by column, rows bottom to top (branch-free)
+            if (bulk && c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);  // prefetch the next chunk
             using LaneC = typename std::conditional<P == 2, LaneP2, LaneP1>::type;
             LaneC L;
             if constexpr (P == 2) L = make_lane_p2(cx, cy);
@@ -627,8 +638,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) M[m] = 0.0;
                 for (int dd = 0; dd < sd.nd; ++dd) {
-                    const DirConst* D = prm.dirs + sd.d0 + dd;
-                    const double coef = (f < 6) ? __ldg(&D->mom[f]) : (((f - 6) & 1) ? __ldg(&D->jw[face]) : __ldg(&D->bw[face]));
+                    const double coef = coefS[dd * NFIELD + f];
                     const double* Sp = S + ((size_t)el * dset + dd) * NQ;
 #pragma unroll
                     for (int m = 0; m < NQ; ++m) M[m] = fma(coef, Sp[m], M[m]);
@@ -881,7 +891,7 @@ int upload_modal(const ModalConsts& mc) { return (int)cudaMemcpyToSymbol(cM, &mc
 int sweep2d_smem_bytes(int p, int k, int gbk, int dset) {
     const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k), NQ = nq_of(p), NN = (p + 1) * (p + 1);
     const int CT = C * T;
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * dset * NQ) * (int)sizeof(double);
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * dset * NQ + dset * 14) * (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
 int sweep2d_cols_per_chunk(int p, int k) { return cols_per_chunk(p, k); }
