@@ -250,7 +250,10 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 // C columns per chunk (one pipeline step).  K >= 4 lanes carry many groups, so
 // fewer rows keep the x-traces in registers.
 __host__ __device__ constexpr int rows_per_strip(int P, int K) { return K >= 4 ? 2 : (P == 2 ? 4 : 8); }
-__host__ __device__ constexpr int cols_per_chunk(int P, int K) { return K >= 4 ? 8 : 4; }
+#ifndef SWEEP_COLS_K4
+#define SWEEP_COLS_K4 8
+#endif
+__host__ __device__ constexpr int cols_per_chunk(int P, int K) { return K >= 4 ? SWEEP_COLS_K4 : 4; }
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
 
 __device__ __forceinline__ int bnode2d(int face, int idx, int node, int nx, int ny, int np1) {
