@@ -225,6 +225,8 @@ static bool build_modal(ModalConsts& mc, std::string& err) {
         mc.V1re[a] = V[a][1].real();
         mc.V1im[a] = V[a][1].imag();
     }
+    mc.V1re2x = 2.0 * mc.V1re[2];
+    mc.V1im2x = 2.0 * mc.V1im[2];
     // 9x9 real maps; modal reals m = [u00, u01r, u01i, u10r, u10i, u11r, u11i, u12r, u12i]
     const int pairs[5][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {1, 2}};
     for (int k = 0; k < 9; ++k) {

@@ -61,6 +61,17 @@ __device__ __forceinline__ double rcp64(double x) {
     return fma(y, e, y);
 }
 
+// 1/x for the element solves: MUFU seed (rel. err <= 2^-20, measured) + one
+// cubic step -> <= 2 ulp (profiles/rcp_acc.cu); parity needs 1e-11.
+__device__ __forceinline__ double rcp64_fast(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -171,7 +182,7 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     const double m11 = e11s + L.I11s, m12 = e11s + L.I12s;
     // one reciprocal for the five real denominators
     const double p1 = d00 * m01, p2 = p1 * m10, p3 = p2 * m11, p4 = p3 * m12;
-    double inv = rcp64(p4);
+    double inv = rcp64_fast(p4);
     const double i12 = inv * p3;
     inv *= m12;
     const double i11 = inv * p2;
@@ -191,15 +202,40 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     u[7] = (r12r * e11 + r12i * L.I12) * i12;
     u[8] = (r12i * e11 - r12r * L.I12) * i12;
 
-    const double v0 = cM.V0[2], vr = cM.V1re[2], vi = cM.V1im[2];
+    const double v0 = cM.V0[2], vr = cM.V1re[2], vi = cM.V1im[2], vr2 = cM.V1re2x, vi2 = cM.V1im2x;
     const double sr = u[5] + u[7], dr = u[5] - u[7];
     const double si = u[6] + u[8], di = u[6] - u[8];
-    txo[0] = v0 * u[0] + 2.0 * (vr * u[3] - vi * u[4]);
+    txo[0] = v0 * u[0] + vr2 * u[3] - vi2 * u[4];
     txo[1] = v0 * u[1] + vr * sr - vi * si;
     txo[2] = v0 * u[2] + vr * di + vi * dr;
-    tyo[0] = v0 * u[0] + 2.0 * (vr * u[1] - vi * u[2]);
+    tyo[0] = v0 * u[0] + vr2 * u[1] - vi2 * u[2];
     tyo[1] = v0 * u[3] + vr * sr - vi * di;
     tyo[2] = v0 * u[4] + vr * si + vi * dr;
+}
+
+// q^ = (W (x) W) q in the 9 modal reals, factored: W along x for each y-row,
+// then W along y (58 FMA instead of 81).  q[a + 3b], a = x node, b = y node.
+__device__ __forceinline__ void modal_forward(const double (&q)[9], double (&qh)[9]) {
+    double s0[3], s1r[3], s1i[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        s0[b] = cM.W0[0] * q[3 * b] + cM.W0[1] * q[3 * b + 1] + cM.W0[2] * q[3 * b + 2];
+        s1r[b] = cM.W1re[0] * q[3 * b] + cM.W1re[1] * q[3 * b + 1] + cM.W1re[2] * q[3 * b + 2];
+        s1i[b] = cM.W1im[0] * q[3 * b] + cM.W1im[1] * q[3 * b + 1] + cM.W1im[2] * q[3 * b + 2];
+    }
+    qh[0] = cM.W0[0] * s0[0] + cM.W0[1] * s0[1] + cM.W0[2] * s0[2];                 // (0,0)
+    qh[1] = cM.W1re[0] * s0[0] + cM.W1re[1] * s0[1] + cM.W1re[2] * s0[2];           // (0,1) re
+    qh[2] = cM.W1im[0] * s0[0] + cM.W1im[1] * s0[1] + cM.W1im[2] * s0[2];           // (0,1) im
+    qh[3] = cM.W0[0] * s1r[0] + cM.W0[1] * s1r[1] + cM.W0[2] * s1r[2];              // (1,0) re
+    qh[4] = cM.W0[0] * s1i[0] + cM.W0[1] * s1i[1] + cM.W0[2] * s1i[2];              // (1,0) im
+    const double rr = cM.W1re[0] * s1r[0] + cM.W1re[1] * s1r[1] + cM.W1re[2] * s1r[2];
+    const double ii = cM.W1im[0] * s1i[0] + cM.W1im[1] * s1i[1] + cM.W1im[2] * s1i[2];
+    const double ri = cM.W1re[0] * s1i[0] + cM.W1re[1] * s1i[1] + cM.W1re[2] * s1i[2];
+    const double ir = cM.W1im[0] * s1r[0] + cM.W1im[1] * s1r[1] + cM.W1im[2] * s1r[2];
+    qh[5] = rr - ii;   // (1,1) = sum W1 W1
+    qh[6] = ri + ir;
+    qh[7] = rr + ii;   // (1,2) = sum W1 conj(W1)
+    qh[8] = ri - ir;
 }
 
 // ------------------------------------------------------------------ 2-D, p = 1
@@ -230,7 +266,7 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
     const double a0 = st + L.cxy;
     const double al = fma(a0, a0, L.sq);
     const double det = fma(al, al, -L.be2);
-    const double inv = rcp64(det);
+    const double inv = rcp64_fast(det);
     const double ai = al * inv, bi = L.be * inv;
     const double s00 = ai * r00 - bi * r11;
     const double s11 = ai * r11 - bi * r00;
@@ -496,13 +532,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                 }
                 ss[el * GBK + gg] = st;
                 if constexpr (P == 2) {
+                    double qh[9];
+                    modal_forward(qv, qh);
 #pragma unroll
-                    for (int m = 0; m < 9; ++m) {
-                        double acc = 0.0;
-#pragma unroll
-                        for (int kk = 0; kk < 9; ++kk) acc = fma(cM.fwd[m][kk], qv[kk], acc);
-                        qs[((size_t)el * NN + m) * GBK + gg] = acc;
-                    }
+                    for (int m = 0; m < 9; ++m) qs[((size_t)el * NN + m) * GBK + gg] = qh[m];
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < NN; ++kk) qs[((size_t)el * NN + kk) * GBK + gg] = qv[kk];
@@ -570,11 +603,19 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         }
                     }
                 } else {
+                    // L1 is clean for this chunk's columns: the acquire above invalidated it
 #pragma unroll
                     for (int k = 0; k < K; ++k)
 #pragma unroll
                         for (int t = 0; t < NT; ++t)
-                            ty[k][t] = __ldcg(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid);
+                            ty[k][t] = __ldca(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid);
+#ifndef SWEEP_NO_PREFETCH
+                    if (col + 1 < C) {
+#pragma unroll
+                        for (int kt = 0; kt < K * NT; ++kt)
+                            prefetch_l1(ysrc + ((size_t)(ip + 1) * K * NT + kt) * NL + tid);
+                    }
+#endif
                 }
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
