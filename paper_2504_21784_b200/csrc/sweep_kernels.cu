@@ -38,14 +38,14 @@ __constant__ ModalConsts cM;
 
 #ifdef SWEEP_TRACE
 // debug timeline (trace builds only): per task [start, end, waited ns, sm id]
-__device__ long long g_trace[1 << 18][4];
+__device__ long long g_trace[1 << 18][8];
 __device__ __forceinline__ long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 extern "C" int sweep_debug_trace(long long* host, int n) {
-    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 4 * (size_t)n);
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 8 * (size_t)n);
 }
 #endif
 
@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
         const int J = task / prm.n_streams;
         const int s = task - J * prm.n_streams;
 #ifdef SWEEP_TRACE
+        long long t_acc[2] = {0, 0};
         long long t_task0 = 0, t_waited = 0;
         if (tid == 0) t_task0 = gtimer();
 #endif
@@ -508,6 +509,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             const int buf = c & 1;
             double* qs = qsb + (size_t)buf * CT * NN * GBK;
             double* ss = ssb + (size_t)buf * CT * GBK;
+#ifdef SWEEP_TRACE
+            long long tc0 = clock64();
+#endif
             // ---- phase A: finish this chunk's staging in place (the copies were issued
             // one chunk ago; bulk copies complete on the mbarrier each thread waits on)
             if (!bulk && c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);
@@ -567,6 +571,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             __syncthreads();
 
             // ---- phase B: sweep the chunk, column by column, rows bottom to top (branch-free)
+#ifdef SWEEP_TRACE
+            long long tc1 = clock64();
+#endif
             if (bulk && c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);  // prefetch the next chunk
             using LaneC = typename std::conditional<P == 2, LaneP2, LaneP1>::type;
             LaneC L;
@@ -660,6 +667,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                 __threadfence();
                 st_release(prm.progress + (size_t)s * prm.n_strips + J, c + 1);
             }
+#ifdef SWEEP_TRACE
+            long long tc2 = clock64();
+            t_acc[0] += tc1 - tc0;
+            t_acc[1] += tc2 - tc1;
+#endif
 
             // ---- phase C: sum over the CTA's directions with the moment / boundary
             // weights, back to nodal values, write this stream's slab
@@ -737,6 +749,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             g_trace[task][1] = gtimer();
             g_trace[task][2] = t_waited;
             g_trace[task][3] = smid;
+            g_trace[task][4] = t_acc[0];
+            g_trace[task][5] = t_acc[1];
         }
 #endif
     }

@@ -32,10 +32,10 @@ sw.timing(True)
 sw.sweep_run(sig, prob.inv_c_dt, q, fl)
 kt = sw.kernel_times(1)
 ntask = 4096
-buf = (ctypes.c_longlong * (4 * ntask))()
+buf = (ctypes.c_longlong * (8 * ntask))()
 lib.sweep_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 lib.sweep_debug_trace(buf, ntask)
-a = np.array(buf).reshape(-1, 4)
+a = np.array(buf).reshape(-1, 8)
 a = a[a[:, 1] > 0]
 t0 = a[:, 0].min()
 start, end, wait = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, a[:, 2] / 1e3
@@ -43,6 +43,8 @@ dur = end - start
 print(f"kernel {kt[0, 0]:.3f} ms; tasks {len(a)}; streams {st['streams']}; ctas {st['ctas']}")
 print(f"task duration us: mean {dur.mean():.1f} min {dur.min():.1f} max {dur.max():.1f}")
 print(f"wait us per task: mean {wait.mean():.1f} max {wait.max():.1f}; total wait fraction {wait.sum() / dur.sum():.3f}")
+tot_cyc = dur.sum() * 1e-6 * 1.965e9
+print(f"cycles (thread 0): A+wait {a[:, 4].sum() / tot_cyc:.3f}  B {a[:, 5].sum() / tot_cyc:.3f}  rest(C, loop) {1 - (a[:, 4].sum() + a[:, 5].sum()) / tot_cyc:.3f}")
 print(f"last end {end.max():.1f} us; sum(dur)/ctas {dur.sum() / st['ctas']:.1f} us")
 for k in range(0, len(a), max(1, len(a) // 24)):
     print(f"  task {k:5d} sm {a[k, 3]:3d} start {start[k]:9.1f} end {end[k]:9.1f} wait {wait[k]:8.1f}")
