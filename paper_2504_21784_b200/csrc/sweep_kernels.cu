@@ -462,6 +462,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
         stage(0, 0);
         // phase-C weights of this stream's directions: [dd][14]
         double* coefS = S + (size_t)CT * dset * NQ;
+        double* ypre = coefS + dset * NFIELD;  // [K*NT][NL] next-column trace prefetch
         for (int it = tid; it < dset * NFIELD; it += NL) {
             const int dd = it / NFIELD, f = it - dd * NFIELD;
             double v = 0.0;
@@ -609,20 +610,40 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                             ty[k][1] = t[1];
                         }
                     }
-                } else {
-                    // L1 is clean for this chunk's columns: the acquire above invalidated it
+                }
+#ifdef SWEEP_ABL_NOYTR
+                else {
 #pragma unroll
                     for (int k = 0; k < K; ++k)
 #pragma unroll
-                        for (int t = 0; t < NT; ++t)
-                            ty[k][t] = __ldca(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid);
-#ifndef SWEEP_NO_PREFETCH
+                        for (int t = 0; t < NT; ++t) ty[k][t] = 0.5;
+                }
+                if (false) {
+#else
+                else {
+#endif
+                    // this lane's traces of column ip: column 0 of a chunk straight from L2
+                    // (issued after this chunk's acquire), later columns from the private
+                    // shared-memory slots the previous column prefetched with cp.async
+                    if (col == 0) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+#pragma unroll
+                            for (int t = 0; t < NT; ++t)
+                                ty[k][t] = __ldcg(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid);
+                    } else {
+                        cp_async_wait<0>();
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+#pragma unroll
+                            for (int t = 0; t < NT; ++t) ty[k][t] = ypre[(k * NT + t) * NL + tid];
+                    }
                     if (col + 1 < C) {
 #pragma unroll
                         for (int kt = 0; kt < K * NT; ++kt)
-                            prefetch_l1(ysrc + ((size_t)(ip + 1) * K * NT + kt) * NL + tid);
+                            cp_async8(ypre + kt * NL + tid, ysrc + ((size_t)(ip + 1) * K * NT + kt) * NL + tid, 8);
+                        cp_async_commit();
                     }
-#endif
                 }
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
@@ -652,7 +673,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                     if (lane == 0) Sd[0] = us[0] + us[1] + us[2] + us[3] + us[NQ - 1];
 #endif
                 }
+#ifdef SWEEP_ABL_NOYTR
+                if (false) {
+#else
                 if (write_y) {
+#endif
 #pragma unroll
                     for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -949,7 +974,8 @@ int upload_modal(const ModalConsts& mc) { return (int)cudaMemcpyToSymbol(cM, &mc
 int sweep2d_smem_bytes(int p, int k, int gbk, int dset) {
     const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k), NQ = nq_of(p), NN = (p + 1) * (p + 1);
     const int CT = C * T;
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * dset * NQ + dset * 14) * (int)sizeof(double);
+    const int NL = dset * gbk / k;  // threads per CTA
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * dset * NQ + dset * 14 + k * (p + 1) * NL) * (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
 int sweep2d_cols_per_chunk(int p, int k) { return cols_per_chunk(p, k); }

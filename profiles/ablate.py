@@ -17,7 +17,8 @@ variants = {"base": [], "nowait": ["-DSWEEP_ABL_NOWAIT"], "nored": ["-DSWEEP_ABL
             "nowait_noC": ["-DSWEEP_ABL_NOWAIT", "-DSWEEP_ABL_NOPHASEC"],
             "nowait_nored": ["-DSWEEP_ABL_NOWAIT", "-DSWEEP_ABL_NORED"],
             "c4": ["-DSWEEP_COLS_K4=4"], "c16": ["-DSWEEP_COLS_K4=16"], "c4_nowait": ["-DSWEEP_COLS_K4=4", "-DSWEEP_ABL_NOWAIT"],
-            "noprefetch": ["-DSWEEP_NO_PREFETCH"], "c2defer": ["-DSWEEP_C2_DEFER"]}
+            "noprefetch": ["-DSWEEP_NO_PREFETCH"], "noytr": ["-DSWEEP_ABL_NOYTR"], "noytr_nowait": ["-DSWEEP_ABL_NOYTR", "-DSWEEP_ABL_NOWAIT"],
+            "nowait_noC_nored_noytr": ["-DSWEEP_ABL_NOYTR", "-DSWEEP_ABL_NOWAIT", "-DSWEEP_ABL_NOPHASEC", "-DSWEEP_ABL_NORED"]}
 if len(sys.argv) > 2:
     variants = {k: v for k, v in variants.items() if k in sys.argv[2].split(",")}
 import numpy as np  # noqa: E402
