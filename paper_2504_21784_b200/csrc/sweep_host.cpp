@@ -10,6 +10,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -417,6 +418,18 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->kpl = 1;
         h->gb = gbw;
         h->log2gb = ilog2_ceil(gbw);
+    }
+    // experiment override (2-D only): SWEEP_CFG="K,LG" with K in {1,2,4}, LG a power of two <= 32
+    if (D.dim == 2) {
+        if (const char* ev = getenv("SWEEP_CFG")) {
+            int k = 0, lg = 0;
+            if (sscanf(ev, "%d,%d", &k, &lg) == 2 && (k == 1 || k == 2 || k == 4) && lg >= 1 && lg <= 32 &&
+                (lg & (lg - 1)) == 0) {
+                h->kpl = k;
+                h->gb = lg;
+                h->log2gb = ilog2_ceil(lg);
+            }
+        }
     }
     const int gbk = h->gb * h->kpl;
     const int n_gblocks = (h->G + gbk - 1) / gbk;

@@ -285,11 +285,12 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 // Strip / chunk geometry as a function of (P, K): T element rows per strip,
 // C columns per chunk (one pipeline step).  K >= 4 lanes carry many groups, so
 // fewer rows keep the x-traces in registers.
-__host__ __device__ constexpr int rows_per_strip(int P, int K) { return K >= 4 ? 2 : (P == 2 ? 4 : 8); }
+__host__ __device__ constexpr int rows_per_strip(int P, int K) { return K >= 4 ? 2 : (K == 2 ? 4 : (P == 2 ? 4 : 8)); }
 #ifndef SWEEP_COLS_K4
 #define SWEEP_COLS_K4 8
 #endif
 __host__ __device__ constexpr int cols_per_chunk(int P, int K) { return K >= 4 ? SWEEP_COLS_K4 : 4; }
+// (K = 2: T = 4 rows, C = 4 columns -> 16 elements per chunk, like K = 4)
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
 
 __device__ __forceinline__ int bnode2d(int face, int idx, int node, int nx, int ny, int np1) {
@@ -961,8 +962,8 @@ static const void* pick2d_k(int log2lg) {
     }
 }
 static const void* pick2d(int p, int log2lg, int k) {
-    if (p == 2) return (k == 4) ? pick2d_k<2, 4>(log2lg) : pick2d_k<2, 1>(log2lg);
-    return (k == 4) ? pick2d_k<1, 4>(log2lg) : pick2d_k<1, 1>(log2lg);
+    if (p == 2) return (k == 4) ? pick2d_k<2, 4>(log2lg) : (k == 2) ? pick2d_k<2, 2>(log2lg) : pick2d_k<2, 1>(log2lg);
+    return (k == 4) ? pick2d_k<1, 4>(log2lg) : (k == 2) ? pick2d_k<1, 2>(log2lg) : pick2d_k<1, 1>(log2lg);
 }
 template <int P>
 static const void* pick1d() {

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 from paper_2504_21784_b200 import build as B  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
-variants = {"base": [], "nowait": ["-DSWEEP_ABL_NOWAIT"], "nored": ["-DSWEEP_ABL_NORED"],
+variants = {"base": [], "cfg2_16": [], "cfg2_32": [], "cfg4_16": [], "cfg4_8": [], "nowait": ["-DSWEEP_ABL_NOWAIT"], "nored": ["-DSWEEP_ABL_NORED"],
             "nophaseC": ["-DSWEEP_ABL_NOPHASEC"],
             "all3": ["-DSWEEP_ABL_NOWAIT", "-DSWEEP_ABL_NORED", "-DSWEEP_ABL_NOPHASEC"],
             "nowait_noC": ["-DSWEEP_ABL_NOWAIT", "-DSWEEP_ABL_NOPHASEC"],
@@ -37,6 +37,9 @@ for name, flags in variants.items():
     subprocess.check_call(cmd)
     S._lib = None
     S.load_library(so)
+    os.environ.pop("SWEEP_CFG", None)
+    if name.startswith("cfg"):
+        os.environ["SWEEP_CFG"] = name[3:].replace("_", ",")
     sw = S.from_problem(prob)
     for _ in range(3):
         sw.sweep_run(sig, prob.inv_c_dt, q, fl)
