@@ -328,6 +328,40 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// L2 eviction-priority policies: streamed inputs are evict-first (each quadrant
+// re-reads them much later), the strip-boundary trace ring is evict-last (read
+// back by the next strip soon).
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_hint(const double* p, unsigned long long pol) {
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc, unsigned long long pol) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "l"(pol) : "memory");
+}
+
 // Lane layout: LG = 2^LOG2LG consecutive lanes share one direction and hold
 // consecutive groups; each lane carries K groups (g, g + LG, ...), so a stream
 // (CTA) covers GBK = LG*K groups of NL/LG directions.  The K independent solves
@@ -377,6 +411,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
         fence_proxy_async();
     }
     unsigned phase_bits = 0;  // parity of the next completion of mbar[0] (bit 0) and mbar[1] (bit 1)
+    const unsigned long long pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
     for (;;) {
         if (tid == 0) s_task = atomicAdd(prm.task_counter, 1);
@@ -426,10 +461,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
                         const size_t e = (size_t)i + (size_t)nx * j;
                         if (kk < NN)
-                            bulk_g2s(qd + ((size_t)el * NN + kk) * GBK, prm.q + (e * NN + kk) * G + sd.g0, row_bytes,
-                                     &mbar[b]);
+                            bulk_g2s_hint(qd + ((size_t)el * NN + kk) * GBK, prm.q + (e * NN + kk) * G + sd.g0,
+                                          row_bytes, &mbar[b], pol_first);
                         else
-                            bulk_g2s(sdst + (size_t)el * GBK, prm.sigma + e * G + sd.g0, row_bytes, &mbar[b]);
+                            bulk_g2s_hint(sdst + (size_t)el * GBK, prm.sigma + e * G + sd.g0, row_bytes, &mbar[b],
+                                          pol_first);
                     }
                 }
             } else {
@@ -631,7 +667,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         for (int k = 0; k < K; ++k)
 #pragma unroll
                             for (int t = 0; t < NT; ++t)
-                                ty[k][t] = __ldcg(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid);
+                                ty[k][t] = ld_hint(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid, pol_last);
                     } else {
                         cp_async_wait<0>();
 #pragma unroll
@@ -642,7 +678,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                     if (col + 1 < C) {
 #pragma unroll
                         for (int kt = 0; kt < K * NT; ++kt)
-                            cp_async8(ypre + kt * NL + tid, ysrc + ((size_t)(ip + 1) * K * NT + kt) * NL + tid, 8);
+                            cp_async8_hint(ypre + kt * NL + tid, ysrc + ((size_t)(ip + 1) * K * NT + kt) * NL + tid,
+                                           pol_last);
                         cp_async_commit();
                     }
                 }
@@ -683,7 +720,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                     for (int k = 0; k < K; ++k)
 #pragma unroll
                         for (int t = 0; t < NT; ++t)
-                            __stcg(ydst + ((size_t)ip * K + k) * NT * NL + t * NL + tid, ty[k][t]);
+                            st_hint(ydst + ((size_t)ip * K + k) * NT * NL + t * NL + tid, ty[k][t], pol_last);
                 }
             }
             // this buffer is refilled by the async proxy two chunks from now
