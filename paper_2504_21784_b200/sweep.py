@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsweep.so")
+LIB_PATH = os.environ.get("SWEEP_LIB") or os.path.join(_HERE, "libsweep.so")  # SWEEP_LIB: experiment builds only
 
 SWEEP_OK, E_ARG, E_QUAD, E_SIGMA, E_CUDA, E_NCCL, E_INTERNAL = range(7)
 FOLD_Z = 1

@@ -85,6 +85,20 @@ def test_fold_z_equivalence(lib):
     assert_parity(b, ref, 2, 24, 24, 1)
 
 
+# ------------------------------------------------------------------ many-group layout
+# G >= 64, p = 2: 16 lanes x 4 groups per direction (the C5 bench layout), bulk copies
+# (G even) or per-element async copies (G odd).  Shapes span several strips / chunks / flag groups
+# with ragged tails, meshes smaller than one chunk, and partial group blocks.
+MANY = [(1, 1, 64, 4), (3, 2, 64, 8), (13, 7, 64, 8), (9, 17, 66, 4), (33, 5, 130, 8), (6, 11, 65, 4), (2, 9, 128, 8)]
+
+
+@pytest.mark.parametrize("nx,ny,G,npol", MANY)
+def test_many_group_layout(lib, nx, ny, G, npol):
+    om, w = synth.product_set(npol, 16)
+    prob = random_problem(700 + nx * ny + G, 2, nx, ny, 2, len(w), G, omega=om, w=w)
+    check(lib, prob)
+
+
 # ------------------------------------------------------------------ configs
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_config_full(lib, cfg):
