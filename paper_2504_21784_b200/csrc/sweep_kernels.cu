@@ -399,7 +399,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
     extern __shared__ __align__(128) double smem[];
     double* qsb = smem;                      // [2][CT][NN][GBK]  (double buffer; modal in place for p=2)
     double* ssb = qsb + 2 * CT * NN * GBK;   // [2][CT][GBK]
-    double* S = ssb + 2 * CT * GBK;          // [CT][dset][NQ]
+    double* S = ssb + 2 * CT * GBK;          // [CT][SEL]: per element [dset][NQ] + 1 pad
+    const int SEL = dset * NQ + 1;           // odd element stride: phase-C reads of two elements hit different banks
     __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ int s_task;
 
@@ -498,8 +499,18 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
         };
         stage(0, 0);
         // phase-C weights of this stream's directions: [dd][14]
-        double* coefS = S + (size_t)CT * dset * NQ;
+        double* coefS = S + (size_t)CT * SEL;
         double* ypre = coefS + dset * NFIELD;  // [K*NT][NL] next-column trace prefetch
+        double* Mbuf = ypre + K * NT * NL;     // [CT][6][NQ] direction sums (phase C stage 1, p = 2)
+        double* bckS = Mbuf + CT * 6 * NQ;     // [9][9] modal -> nodal (p = 2)
+        // (compile-time constant-bank indices only: ptxas hoists constant loads out of
+        // the task loop for every thread, and a thread-dependent index past the end of
+        // the constant bank is a fatal illegal instruction)
+        if constexpr (P == 2)
+            if (tid == 0) {
+#pragma unroll
+                for (int it = 0; it < 81; ++it) bckS[it] = cM.bck[it / 9][it % 9];
+            }
         for (int it = tid; it < dset * NFIELD; it += NL) {
             const int dd = it / NFIELD, f = it - dd * NFIELD;
             double v = 0.0;
@@ -510,6 +521,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             coefS[it] = v;
         }
 
+        bool y0_pref = false;  // J == 0: ypre holds the next column's raw y-inflow
         // x-inflow traces of the strip (domain boundary at i' = 0)
         double tx[K][T][NT];
 #pragma unroll
@@ -626,25 +638,56 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                 const int ip = i0 + col;
                 double ty[K][NT];
                 if (J == 0) {
-                    const bool col_on = ip < nx;
-                    const int i = fx ? nx - 1 - ip : ip;
+                    // bottom strip: the y-inflow of column ip (raw nodal values, prefetched
+                    // into ypre while column ip-1 was swept; it has no dependency, so the
+                    // prefetch also crosses chunk boundaries), then to modal form.  Loading it
+                    // on demand put an L2 round trip on every column of the strip that heads
+                    // the whole pipeline.
+                    auto inflow_addr = [&](int ipc, int k, int aq, bool& on) -> const double* {
+                        const int i = fx ? nx - 1 - ipc : ipc;
+                        const int a = fx ? P - aq : aq;
+                        on = ipc < nx && (gl + k * LG < sd.ng);
+                        return on ? prm.inflow + (size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + sd.g0 + gl + k * LG
+                                  : prm.inflow;
+                    };
+                    double t[K][NP1];
+                    if (y0_pref) {
+                        cp_async_wait<0>();
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+#pragma unroll
+                            for (int aq = 0; aq < NP1; ++aq) t[k][aq] = ypre[(k * NP1 + aq) * NL + tid];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+#pragma unroll
+                            for (int aq = 0; aq < NP1; ++aq) {
+                                bool on;
+                                const double* a = inflow_addr(ip, k, aq, on);
+                                t[k][aq] = on ? *a : 0.0;
+                            }
+                    }
+                    y0_pref = ip + 1 < nx;
+                    if (y0_pref) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+#pragma unroll
+                            for (int aq = 0; aq < NP1; ++aq) {
+                                bool on;
+                                const double* a = inflow_addr(ip + 1, k, aq, on);
+                                cp_async8(ypre + (k * NP1 + aq) * NL + tid, a, on ? 8 : 0);
+                            }
+                        cp_async_commit();
+                    }
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        const bool on = col_on && (gl + k * LG < sd.ng);
-                        const int g = sd.g0 + gl + k * LG;
-                        double t[NP1];
-#pragma unroll
-                        for (int aq = 0; aq < NP1; ++aq) {
-                            const int a = fx ? P - aq : aq;
-                            t[aq] = on ? prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g] : 0.0;
-                        }
                         if constexpr (P == 2) {
-                            ty[k][0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
-                            ty[k][1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
-                            ty[k][2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
+                            ty[k][0] = cM.W0[0] * t[k][0] + cM.W0[1] * t[k][1] + cM.W0[2] * t[k][2];
+                            ty[k][1] = cM.W1re[0] * t[k][0] + cM.W1re[1] * t[k][1] + cM.W1re[2] * t[k][2];
+                            ty[k][2] = cM.W1im[0] * t[k][0] + cM.W1im[1] * t[k][1] + cM.W1im[2] * t[k][2];
                         } else {
-                            ty[k][0] = t[0];
-                            ty[k][1] = t[1];
+                            ty[k][0] = t[k][0];
+                            ty[k][1] = t[k][1];
                         }
                     }
                 }
@@ -703,7 +746,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
 #pragma unroll
                         for (int m = 0; m < NQ; ++m) us[m] = (k == 0) ? u[m] : us[m] + u[m];
                     }
-                    double* Sd = S + ((size_t)el * dset + dl) * NQ;
+                    double* Sd = S + (size_t)el * SEL + dl * NQ;
                     auto sink = [&](int idx, double val) { Sd[idx] = val; };
 #ifndef SWEEP_ABL_NORED
                     ReduceScatter<NQ, LG / 2>::run(us, lane, 0, NQ, sink);
@@ -737,55 +780,66 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
 #endif
 
             // ---- phase C: sum over the CTA's directions with the moment / boundary
-            // weights, back to nodal values, write this stream's slab
+            // weights, back to nodal values, write this stream's slab.
+            // stage 1: M[el][f][m] = sum_d coef[d][f] S[el][d][m] for the 6 moment fields,
+            //          one output per thread and pass (consecutive threads: consecutive m);
+            //          boundary fields (beta, J+) per (element, face) on boundary elements;
+            // stage 2 (p = 2): nodal psi[el][f][k] = sum_m bck[k][m] M[el][f][m].
 #ifdef SWEEP_ABL_NOPHASEC
-            if (false)
+            if (false) {
+#else
+            {
 #endif
-            for (int it = tid; it < CT * NFIELD; it += NL) {
-                const int el = it / NFIELD, f = it - el * NFIELD;
-                const int col = el / T, r = el - col * T;
-                if (col >= cols || r >= rows) continue;
-                const int ip = i0 + col, jp = j0 + r;
-                const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                int face = -1;
-                if (f >= 6) {
-                    face = (f - 6) >> 1;
+                auto node_store = [&](double* dst, int kk, double v) {
+                    const int aq = kk % NP1, bq = kk / NP1;
+                    const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
+                    dst[a + NP1 * b] = v;
+                };
+                for (int o = tid; o < CT * 6 * NQ; o += NL) {
+                    const int m = o % NQ, rest = o / NQ;
+                    const int f = rest % 6, el = rest / 6;
+                    const double* Sp = S + (size_t)el * SEL + m;
+                    const double* cf = coefS + f;
+                    double a0 = 0.0, a1 = 0.0;
+                    int dd = 0;
+                    for (; dd + 1 < sd.nd; dd += 2) {
+                        a0 = fma(cf[dd * NFIELD], Sp[dd * NQ], a0);
+                        a1 = fma(cf[(dd + 1) * NFIELD], Sp[(dd + 1) * NQ], a1);
+                    }
+                    if (dd < sd.nd) a0 = fma(cf[dd * NFIELD], Sp[dd * NQ], a0);
+                    const double acc = a0 + a1;
+                    if constexpr (P == 2) {
+                        Mbuf[o] = acc;
+                    } else {
+                        const int col = el / T, r = el - col * T;
+                        if (col < cols && r < rows) {
+                            const int ip = i0 + col, jp = j0 + r;
+                            const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                            node_store(slab + (size_t)f * nodes + ((size_t)i + (size_t)nx * j) * NN, m, acc);
+                        }
+                    }
+                }
+                // boundary closures: (element, face) items on physical boundary faces
+                for (int o = tid; o < CT * 4; o += NL) {
+                    const int el = o >> 2, face = o & 3;
+                    const int col = el / T, r = el - col * T;
+                    if (col >= cols || r >= rows) continue;
+                    const int ip = i0 + col, jp = j0 + r;
+                    const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
                     const bool on = (face == 0) ? (i == 0) : (face == 1) ? (i == nx - 1) : (face == 2) ? (j == 0) : (j == ny - 1);
                     if (!on) continue;
-                }
-                double M[NQ];
+                    double Mb[NQ], Mj[NQ];
 #pragma unroll
-                for (int m = 0; m < NQ; ++m) M[m] = 0.0;
-                for (int dd = 0; dd < sd.nd; ++dd) {
-                    const double coef = coefS[dd * NFIELD + f];
-                    const double* Sp = S + ((size_t)el * dset + dd) * NQ;
+                    for (int m = 0; m < NQ; ++m) Mb[m] = Mj[m] = 0.0;
+                    for (int dd = 0; dd < sd.nd; ++dd) {
+                        const double cb = coefS[dd * NFIELD + 6 + 2 * face], cj = coefS[dd * NFIELD + 7 + 2 * face];
+                        const double* Sp = S + (size_t)el * SEL + dd * NQ;
 #pragma unroll
-                    for (int m = 0; m < NQ; ++m) M[m] = fma(coef, Sp[m], M[m]);
-                }
-                double psi[NN];
-                if constexpr (P == 2) {
-#pragma unroll
-                    for (int kk = 0; kk < 9; ++kk) {
-                        double acc = 0.0;
-#pragma unroll
-                        for (int m = 0; m < 9; ++m) acc = fma(cM.bck[kk][m], M[m], acc);
-                        psi[kk] = acc;
+                        for (int m = 0; m < NQ; ++m) {
+                            Mb[m] = fma(cb, Sp[m], Mb[m]);
+                            Mj[m] = fma(cj, Sp[m], Mj[m]);
+                        }
                     }
-                } else {
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) psi[kk] = M[kk];
-                }
-                const size_t e = (size_t)i + (size_t)nx * j;
-                if (f < 6) {
-                    double* dst = slab + (size_t)f * nodes + e * NN;
-#pragma unroll
-                    for (int kk = 0; kk < NN; ++kk) {
-                        const int aq = kk % NP1, bq = kk / NP1;
-                        const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
-                        dst[a + NP1 * b] = psi[kk];
-                    }
-                } else {
-                    double* dst = slab + 6 * nodes + (((f - 6) & 1) ? prm.nbnode : 0);
 #pragma unroll
                     for (int t = 0; t < NP1; ++t) {
                         int a, b, idx;
@@ -798,8 +852,38 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                             a = t;
                             idx = i;
                         }
-                        const int aq = fx ? P - a : a, bq = fy ? P - b : b;
-                        dst[bnode2d(face, idx, t, nx, ny, NP1)] = psi[aq + NP1 * bq];
+                        const int kk = (fx ? P - a : a) + NP1 * (fy ? P - b : b);
+                        double vb = 0.0, vj = 0.0;
+                        if constexpr (P == 2) {
+#pragma unroll
+                            for (int m = 0; m < 9; ++m) {
+                                vb = fma(bckS[kk * 9 + m], Mb[m], vb);
+                                vj = fma(bckS[kk * 9 + m], Mj[m], vj);
+                            }
+                        } else {
+                            vb = Mb[kk];
+                            vj = Mj[kk];
+                        }
+                        const int bn = bnode2d(face, idx, t, nx, ny, NP1);
+                        slab[6 * nodes + bn] = vb;
+                        slab[6 * nodes + prm.nbnode + bn] = vj;
+                    }
+                }
+                if constexpr (P == 2) {
+                    __syncthreads();
+                    for (int o = tid; o < CT * 6 * NN; o += NL) {
+                        const int kk = o % NN, rest = o / NN;
+                        const int f = rest % 6, el = rest / 6;
+                        const int col = el / T, r = el - col * T;
+                        if (col >= cols || r >= rows) continue;
+                        const double* Mp = Mbuf + rest * NQ;
+                        const double* bk = bckS + kk * 9;
+                        double v = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 9; ++m) v = fma(bk[m], Mp[m], v);
+                        const int ip = i0 + col, jp = j0 + r;
+                        const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                        node_store(slab + (size_t)f * nodes + ((size_t)i + (size_t)nx * j) * NN, kk, v);
                     }
                 }
             }
@@ -1013,7 +1097,8 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset) {
     const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k), NQ = nq_of(p), NN = (p + 1) * (p + 1);
     const int CT = C * T;
     const int NL = dset * gbk / k;  // threads per CTA
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * dset * NQ + dset * 14 + k * (p + 1) * NL) * (int)sizeof(double);
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + CT * 6 * NQ + 81) *
+           (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
 int sweep2d_cols_per_chunk(int p, int k) { return cols_per_chunk(p, k); }

@@ -1,0 +1,15 @@
+import sys, os
+sys.path.insert(0, '.')
+import oracle
+from synth.configs import random_problem
+import paper_2504_21784_b200 as pk
+from tests.parity import field_errors
+nx, ny, p, nd, G = map(int, sys.argv[1:6])
+prob = random_problem(507, 2, nx, ny, p, nd, G)
+try:
+    got = pk.run_problem(prob)
+    ref = oracle.sweep(prob)
+    e = field_errors(got, ref, 2, nx, ny, p)
+    print(os.environ.get("SWEEP_LIB", "default"), (nx, ny, p, nd, G), 'max err %.2e' % max(v[0] for v in e.values()), flush=True)
+except Exception as ex:
+    print(os.environ.get("SWEEP_LIB", "default"), (nx, ny, p, nd, G), 'EXC', ex, flush=True)
