@@ -8,7 +8,10 @@ PAPER.md passages each step follows.
 Parity status: pinned (tests/test_oracle_pins.py) — dense global assembly in
 the paper's jump/average form, closed-form 1-D transmission, constant-solution
 exactness, global particle balance, convergence order, rotation symmetry,
-quadrature identities.
+quadrature identities; sigma-weighted moments pinned by their reductions
+(one group, group-constant sigma, constant solution); the fixup pinned by
+the worked element examples and an independent element-by-element sweep in
+the jump/average form (tests/dense_dg.py) on tiny meshes.
 """
 from __future__ import annotations
 
@@ -43,7 +46,13 @@ def _load():
         i, d = ctypes.c_int, ctypes.c_double
         lib.oracle_sweep.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, dp, i]
         lib.oracle_sweep.restype = i
-        lib.oracle_sweep_psi.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, i, i, dp]
+        lib.oracle_sweep2.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, dp, i, i]
+        lib.oracle_sweep2.restype = i
+        lib.oracle_out_size2.argtypes = [i, i, i, i, i]
+        lib.oracle_out_size2.restype = i
+        lib.oracle_fixup.argtypes = [i, dp, dp]
+        lib.oracle_fixup.restype = i
+        lib.oracle_sweep_psi.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, i, i, dp, i]
         lib.oracle_sweep_psi.restype = i
         lib.oracle_alpha.argtypes = [i, i, dp, dp, dp]
         lib.oracle_alpha.restype = None
@@ -61,30 +70,44 @@ def _c(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def out_size(dim: int, nx: int, ny: int, p: int) -> int:
-    return _load().oracle_out_size(dim, nx, ny if dim == 2 else 1, p)
+SIGMA_MOMENTS = 1   # opts bit 0: append sum_g sigma_g phi_g, sum_g sigma_g J_g (NEXT-1)
+FIXUP = 2           # opts bit 1: zero-and-scale negative flux fixup inside the sweep (NEXT-2)
 
 
-def sweep(prob, nthreads: int = 0) -> np.ndarray:
-    """Packed gray output phi|J|T|beta|J+ (same layout as closures_get)."""
+def out_size(dim: int, nx: int, ny: int, p: int, opts: int = 0) -> int:
+    return _load().oracle_out_size2(dim, nx, ny if dim == 2 else 1, p, int(opts))
+
+
+def sweep(prob, nthreads: int = 0, opts: int = 0) -> np.ndarray:
+    """Packed gray output phi|J|T|beta|J+ [|sphi|sJ] (same layout as closures_get)."""
     lib = _load()
     om, w, s, q, fl = _c(prob.omega), _c(prob.w), _c(prob.sigma), _c(prob.q), _c(prob.inflow)
-    out = np.zeros(out_size(prob.dim, prob.nx, prob.ny, prob.p))
-    rc = lib.oracle_sweep(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
-                          s.shape[1], _ptr(s), float(prob.inv_c_dt), _ptr(q), _ptr(fl), _ptr(out), int(nthreads))
+    out = np.zeros(out_size(prob.dim, prob.nx, prob.ny, prob.p, opts))
+    rc = lib.oracle_sweep2(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
+                           s.shape[1], _ptr(s), float(prob.inv_c_dt), _ptr(q), _ptr(fl), _ptr(out), int(nthreads),
+                           int(opts))
     if rc != 0:
         raise RuntimeError(f"oracle_sweep failed rc={rc}")
     return out
 
 
-def sweep_psi(prob, d: int, g: int) -> np.ndarray:
+def fixup(x, W) -> np.ndarray:
+    """The oracle's element-level zero-and-scale fixup applied to a copy of x (weights W)."""
+    lib = _load()
+    x, W = _c(np.array(x, dtype=np.float64)), _c(W)
+    lib.oracle_fixup(x.size, _ptr(W), _ptr(x))
+    return x
+
+
+def sweep_psi(prob, d: int, g: int, opts: int = 0) -> np.ndarray:
     """psi_{d,g} as [N_el][n]."""
     lib = _load()
     om, w, s, q, fl = _c(prob.omega), _c(prob.w), _c(prob.sigma), _c(prob.q), _c(prob.inflow)
     n = (prob.p + 1) ** prob.dim
     psi = np.zeros((prob.nx * (prob.ny if prob.dim == 2 else 1), n))
     rc = lib.oracle_sweep_psi(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
-                              s.shape[1], _ptr(s), float(prob.inv_c_dt), _ptr(q), _ptr(fl), d, g, _ptr(psi))
+                              s.shape[1], _ptr(s), float(prob.inv_c_dt), _ptr(q), _ptr(fl), d, g, _ptr(psi),
+                              int(opts))
     if rc != 0:
         raise RuntimeError(f"oracle_sweep_psi failed rc={rc}")
     return psi
@@ -99,7 +122,7 @@ def alpha(prob) -> np.ndarray:
     return a
 
 
-def unpack(out: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
+def unpack(out: np.ndarray, dim: int, nx: int, ny: int, p: int, opts: int = 0) -> dict:
     """Split a packed output into named fields (oracle side's own layout reader)."""
     n = (p + 1) ** dim
     nel = nx * (ny if dim == 2 else 1)
@@ -113,5 +136,8 @@ def unpack(out: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
     f["T"] = out[o:o + nT * nodes].reshape(nT, nel, n); o += nT * nodes
     f["beta"] = out[o:o + nb]; o += nb
     f["Jplus"] = out[o:o + nb]; o += nb
+    if opts & SIGMA_MOMENTS:
+        f["sphi"] = out[o:o + nodes].reshape(nel, n); o += nodes
+        f["sJ"] = out[o:o + dim * nodes].reshape(dim, nel, n); o += dim * nodes
     assert o == out.size
     return f

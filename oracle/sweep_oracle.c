@@ -21,6 +21,17 @@
  *       beta = sum w (|Omega.n| - alpha) psi  on boundary face nodes
  *       alpha = sum w |Omega.n| / sum w       (eq:alpha PAPER.md:173-175)
  *       J+  = sum_{Omega.n>0} w (Omega.n) psi on boundary face nodes
+ *   Options (opts bit 0): the sigma-weighted gray moments the
+ *   gray low-order system takes from the sweep,
+ *       sphi = sum_g sigma_g phi_g    (numerator of sigma_E, eq:sigmaE PAPER.md:183-185)
+ *       sJ   = sum_g sigma_g J_g      (additive correction sum_g (sigma_F - sigma_g) F_g,
+ *                                      eq:additive_mg_correction PAPER.md:197-203, :247)
+ *   with sigma_g the opacity WITHOUT the 1/(c dt) pseudo-absorption.
+ *   (opts bit 1): the zero-and-scale negative flux fixup inside the
+ *   sweep: after each element solve, if a nodal value is
+ *   negative, negatives are set to 0 and the rest scaled so the element integral
+ *   sum_k W_k psi_k is preserved; a non-positive integral zeroes the element.  The
+ *   fixed-up values are what the downwind elements see.
  *
  * How (deliberately plain): for each (d,g), elements are visited in upwind
  * nested-loop order; the element matrix is assembled UNSCALED straight from
@@ -133,6 +144,31 @@ static int lu_solve(int n, double *A, double *r, double *x) {
 }
 
 /*
+ * Zero-and-scale fixup of one element's nodal values x[n] with lumped-mass
+ * weights W[n] ("zero and scale negative flux fixup ... preserving
+ * particle balance"; reading F1 in DESIGN.md: the preserved quantity is the
+ * element integral sum_k W_k x_k).  Returns 1 if x was changed.
+ */
+int oracle_fixup(int n, const double *W, double *x) {
+    int neg = 0;
+    for (int k = 0; k < n; ++k)
+        if (x[k] < 0.0) neg = 1;
+    if (!neg) return 0;
+    double total = 0.0, pos = 0.0;
+    for (int k = 0; k < n; ++k) {
+        total += W[k] * x[k];
+        if (x[k] > 0.0) pos += W[k] * x[k];
+    }
+    if (total <= 0.0) {
+        for (int k = 0; k < n; ++k) x[k] = 0.0;
+        return 1;
+    }
+    const double scale = total / pos;
+    for (int k = 0; k < n; ++k) x[k] = (x[k] > 0.0) ? x[k] * scale : 0.0;
+    return 1;
+}
+
+/*
  * One (d,g) sweep.  psi [N_el][n].  Returns 0, or -1 on a singular block.
  * Weak form per element K, test function l_k (eq:dgsn_transport with the
  * upwind flux):
@@ -143,7 +179,7 @@ static int lu_solve(int n, double *A, double *r, double *x) {
  * int_f f = sum over face nodes of (face weight) f; grad l_k at node l =
  * (D_{a_l a_k}/hx delta_{b_k b_l}, D_{b_l b_k}/hy delta_{a_k a_l}).
  */
-static int sweep_dg(const prob *P, int d, int g, double *psi) {
+static int sweep_dg(const prob *P, int d, int g, double *psi, int fixup) {
     const int nx = P->nx, ny = P->ny, np1 = P->np1, n = P->n, G = P->G;
     const double ox = P->omega[3 * d + 0], oy = (P->dim == 2) ? P->omega[3 * d + 1] : 0.0;
     const double hx = P->hx, hy = P->hy;
@@ -221,6 +257,7 @@ static int sweep_dg(const prob *P, int d, int g, double *psi) {
                 }
             }
             if (lu_solve(n, A, r, x) != 0) return -1;
+            if (fixup) oracle_fixup(n, W, x);
             for (int k = 0; k < n; ++k) psi[(size_t)e * n + k] = x[k];
         }
     }
@@ -251,20 +288,23 @@ static int setup(prob *P, int dim, int nx, int ny, double lx, double ly, int p, 
     return 0;
 }
 
-/* number of output doubles: phi, J(dim), T(1 or 3) per node; beta, J+ per boundary node */
-static size_t out_size(const prob *P, size_t *nodes, int *nT) {
+/* number of output doubles: phi, J(dim), T(1 or 3) per node; beta, J+ per boundary
+ * node; with opts bit 0 also sphi, sJ(dim) per node */
+static size_t out_size(const prob *P, size_t *nodes, int *nT, int opts) {
     *nodes = (size_t)P->nx * P->ny * P->n;
     *nT = (P->dim == 1) ? 1 : 3;
-    return (*nodes) * (1 + P->dim + *nT) + 2 * (size_t)P->nbnode;
+    return (*nodes) * (1 + P->dim + *nT) + 2 * (size_t)P->nbnode + ((opts & 1) ? (*nodes) * (1 + P->dim) : 0);
 }
 
-int oracle_out_size(int dim, int nx, int ny, int p) {
+int oracle_out_size2(int dim, int nx, int ny, int p, int opts) {
     int n = (dim == 2) ? (p + 1) * (p + 1) : p + 1;
     int nel = (dim == 2) ? nx * ny : nx;
     int nT = (dim == 1) ? 1 : 3;
     int nb = (dim == 1) ? 2 : 2 * (nx + ny) * (p + 1);
-    return nel * n * (1 + dim + nT) + 2 * nb;
+    return nel * n * (1 + dim + nT) + 2 * nb + ((opts & 1) ? nel * n * (1 + dim) : 0);
 }
+
+int oracle_out_size(int dim, int nx, int ny, int p) { return oracle_out_size2(dim, nx, ny, p, 0); }
 
 /* alpha_n = sum_d w_d |Omega_d . n| / sum_d w_d for n in {x-, x+, y-, y+} (eq:alpha) */
 void oracle_alpha(int dim, int ndir, const double *omega, const double *w, double *alpha4) {
@@ -282,30 +322,34 @@ void oracle_alpha(int dim, int ndir, const double *omega, const double *w, doubl
 int oracle_sweep_psi(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
                      const double *omega, const double *w, int G, const double *sigma,
                      double inv_c_dt, const double *q, const double *inflow, int d, int g,
-                     double *psi_out) {
+                     double *psi_out, int opts) {
     prob P;
     int rc = setup(&P, dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, inv_c_dt, q, inflow);
     if (rc) return rc;
     if (d < 0 || d >= ndir || g < 0 || g >= G) return -2;
-    return sweep_dg(&P, d, g, psi_out);
+    return sweep_dg(&P, d, g, psi_out, (opts >> 1) & 1);
 }
 
 /*
  * Full sweep + gray moments.  out layout (packed, as the C-ABI's closures_get):
  *   phi[N_el][n] | J[dim][N_el][n] | T[nT][N_el][n] | beta[N_bnode] | Jplus[N_bnode]
+ *   [ | sphi[N_el][n] | sJ[dim][N_el][n]   when opts bit 0 ]
+ * opts bit 1: zero-and-scale fixup inside the sweep.
  * nthreads <= 0: OpenMP default.  Returns 0, -1 singular block, -2 bad args, -3 OOM.
  */
-int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
-                 const double *omega, const double *w, int G, const double *sigma,
-                 double inv_c_dt, const double *q, const double *inflow, double *out,
-                 int nthreads) {
+int oracle_sweep2(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
+                  const double *omega, const double *w, int G, const double *sigma,
+                  double inv_c_dt, const double *q, const double *inflow, double *out,
+                  int nthreads, int opts) {
     prob P;
     int rc = setup(&P, dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, inv_c_dt, q, inflow);
     if (rc) return rc;
     size_t nodes;
     int nT;
-    const size_t nout = out_size(&P, &nodes, &nT);
+    const size_t nout = out_size(&P, &nodes, &nT, opts);
     const int ncomp = 1 + dim + nT;
+    const int sig_mom = opts & 1, fixup = (opts >> 1) & 1;
+    const size_t off_sig = (size_t)ncomp * nodes + 2 * (size_t)P.nbnode;  /* sphi, then sJ */
 
     /* per-direction closure coefficients, precomputed as w (Omega Omega - I/3) (R16) */
     double *coef = (double *)malloc(sizeof(double) * (size_t)ndir * 6);
@@ -377,7 +421,7 @@ int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
         for (long pr = 0; pr < npairs; ++pr) {
             if (!psi) continue;
             const int d = (int)(pr / G), g = (int)(pr % G);
-            if (sweep_dg(&P, d, g, psi) != 0) {
+            if (sweep_dg(&P, d, g, psi, fixup) != 0) {
 #pragma omp atomic write
                 fail = -1;
                 continue;
@@ -386,6 +430,17 @@ int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
             for (size_t v = 0; v < nodes; ++v) {
                 const double ps = psi[v];
                 for (int m = 0; m < ncomp; ++m) nadd(&S[m * nodes + v], &C[m * nodes + v], c[m] * ps);
+            }
+            if (sig_mom) {
+                /* sum_g sigma_g (w, w Omega) psi: sigma_g of the node's element, no 1/(c dt) */
+                for (size_t v = 0; v < nodes; ++v) {
+                    const double sg = P.sigma[(v / P.n) * G + g];
+                    const double ps = psi[v];
+                    for (int m = 0; m <= dim; ++m) {
+                        const size_t o = off_sig + m * nodes + v;
+                        nadd(&S[o], &C[o], sg * (c[m] * ps));
+                    }
+                }
             }
             const double ox = omega[3 * d], oy = (dim == 2) ? omega[3 * d + 1] : 0.0;
             for (int t = 0; t < nb; ++t) {
@@ -417,4 +472,11 @@ int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
     }
     free(acc); free(coef); free(b_el); free(b_k); free(b_f);
     return fail;
+}
+
+int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
+                 const double *omega, const double *w, int G, const double *sigma,
+                 double inv_c_dt, const double *q, const double *inflow, double *out,
+                 int nthreads) {
+    return oracle_sweep2(dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, inv_c_dt, q, inflow, out, nthreads, 0);
 }

@@ -36,8 +36,8 @@ def _dmat(xi: np.ndarray) -> np.ndarray:
     return dV @ C
 
 
-def solve_global(prob, d: int, g: int) -> np.ndarray:
-    """psi_{d,g} [N_el][n] from one dense solve of the assembled global system."""
+def assemble_global(prob, d: int, g: int):
+    """(A, b) of the global system for (d, g), unknowns ordered (element, node)."""
     dim, p = prob.dim, prob.p
     nx = prob.nx
     ny = prob.ny if dim == 2 else 1
@@ -116,5 +116,57 @@ def solve_global(prob, d: int, g: int) -> np.ndarray:
                 A[k1, k1] += wf * on                          # Gamma_b^+: Omega.n u psi
             elif on < 0:
                 b[k1] -= wf * on * prob.inflow[bn, g]        # - int_{Gamma_b^-} Omega.n u psi_in
-    psi = np.linalg.solve(A, b)
+    return A, b
+
+
+def solve_global(prob, d: int, g: int) -> np.ndarray:
+    """psi_{d,g} [N_el][n] from one dense solve of the assembled global system."""
+    A, b = assemble_global(prob, d, g)
+    nel = prob.nx * (prob.ny if prob.dim == 2 else 1)
+    return np.linalg.solve(A, b).reshape(nel, -1)
+
+
+def element_weights(prob) -> np.ndarray:
+    """Lumped mass weights W_k of one element (tensor GLL)."""
+    _, wh = _gll(prob.p)
+    hx = prob.lx / prob.nx
+    if prob.dim == 1:
+        return hx * wh
+    hy = prob.ly / prob.ny
+    return hx * hy * np.outer(wh, wh).reshape(-1)   # k = a + (p+1) b  ->  wh[b] * wh[a]
+
+
+def zero_and_scale(x: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """Zero-and-scale fixup (SPEC.md's fixup_zero_and_scale): negatives to
+    0, the rest scaled so sum W x is kept; a non-positive sum zeroes the element."""
+    if (x >= 0).all():
+        return x
+    total = float(W @ x)
+    if total <= 0:
+        return np.zeros_like(x)
+    pos = np.where(x > 0, x, 0.0)
+    return pos * (total / float(W @ pos))
+
+
+def sweep_blocks(prob, d: int, g: int, fixup: bool = True) -> np.ndarray:
+    """Element-by-element block forward substitution of the global system in upwind
+    order, with the fixup applied to each element before its downwind neighbours use
+    it (the sweep of PAPER.md:987 written on the jump/average assembly)."""
+    A, b = assemble_global(prob, d, g)
+    nx = prob.nx
+    ny = prob.ny if prob.dim == 2 else 1
+    n = A.shape[0] // (nx * ny)
+    ox = prob.omega[d, 0]
+    oy = prob.omega[d, 1] if prob.dim == 2 else 0.0
+    W = element_weights(prob)
+    psi = np.zeros(A.shape[0])
+    jr = range(ny) if oy >= 0 else range(ny - 1, -1, -1)
+    for j in jr:
+        ir = range(nx) if ox >= 0 else range(nx - 1, -1, -1)
+        for i in ir:
+            e = i + nx * j
+            sl = slice(e * n, (e + 1) * n)
+            r = b[sl] - A[sl, :] @ psi + A[sl, sl] @ psi[sl]
+            x = np.linalg.solve(A[sl, sl], r)
+            psi[sl] = zero_and_scale(x, W) if fixup else x
     return psi.reshape(nx * ny, n)

@@ -1,0 +1,137 @@
+"""Pins for the oracle's NEXT rows (-m "not gpu"):
+  NEXT-1  sigma-weighted gray moments sum_g sigma_g phi_g, sum_g sigma_g J_g
+          (eq:sigmaE PAPER.md:183-185, additive MG correction :197-203, :247);
+  NEXT-2  zero-and-scale negative flux fixup inside the sweep.
+Each pin compares the oracle with something other than itself: an independent
+psi (dense global / block assembly in the jump/average form, tests/dense_dg.py),
+worked element examples (SPEC.md's fixup examples), or reductions the
+definitions fix (one group, group-constant sigma, the constant solution)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth.configs import Problem, random_problem
+from tests.dense_dg import solve_global, sweep_blocks
+
+SIG, FIX = oracle.SIGMA_MOMENTS, oracle.FIXUP
+
+
+# ------------------------------------------------------------------ NEXT-1
+@pytest.mark.parametrize("dim,p", [(1, 1), (1, 2), (2, 1), (2, 2)])
+def test_sigma_moments_from_independent_psi(dim, p):
+    """sphi = sum_g sigma_g sum_d w psi, sJ = sum_g sigma_g sum_d w Omega psi with psi
+    from the dense global solve (not the oracle's sweep)."""
+    nx, ny = (5, 1) if dim == 1 else (3, 2)
+    prob = random_problem(40 + 3 * dim + p, dim, nx, ny, p, 5, 3)
+    f = oracle.unpack(oracle.sweep(prob, opts=SIG), dim, nx, ny, p, opts=SIG)
+    sphi = np.zeros_like(f["sphi"])
+    sJ = np.zeros_like(f["sJ"])
+    for d in range(prob.n_dir):
+        for g in range(prob.G):
+            psi = solve_global(prob, d, g)
+            sg = prob.sigma[:, g][:, None]
+            sphi += sg * prob.w[d] * psi
+            for c in range(dim):
+                sJ[c] += sg * prob.w[d] * prob.omega[d, c] * psi
+    scale = np.abs(sphi).max()
+    assert np.abs(f["sphi"] - sphi).max() < 1e-13 * scale
+    assert np.abs(f["sJ"] - sJ).max() < 1e-13 * scale
+
+
+@pytest.mark.parametrize("dim,p", [(1, 2), (2, 1)])
+def test_sigma_moments_group_constant_sigma(dim, p):
+    """sigma_g = s_e for every group => sphi = s_e phi, sJ = s_e J (per element)."""
+    nx, ny = (6, 1) if dim == 1 else (4, 3)
+    prob = random_problem(61, dim, nx, ny, p, 6, 4)
+    s_e = np.exp(np.random.default_rng(3).uniform(-2, 3, size=prob.sigma.shape[0]))
+    prob.sigma[:] = s_e[:, None]
+    f = oracle.unpack(oracle.sweep(prob, opts=SIG), dim, nx, ny, p, opts=SIG)
+    assert np.abs(f["sphi"] - s_e[:, None] * f["phi"]).max() < 1e-13 * np.abs(f["sphi"]).max()
+    assert np.abs(f["sJ"] - s_e[None, :, None] * f["J"]).max() < 1e-13 * np.abs(f["sphi"]).max()
+
+
+def test_sigma_moments_constant_solution():
+    """psi == Q_g (constant solution) => sphi = sum_g sigma_g Q_g per node (sigma_t:
+    the 1/(c dt) pseudo-absorption is not an opacity), sJ = 0."""
+    nx, ny, p, G = 4, 3, 2, 3
+    om, w = synth.product_set(4, 8)
+    rng = np.random.default_rng(8)
+    ne, n = nx * ny, 9
+    sig = rng.uniform(0.5, 50.0, size=(ne, G))
+    Q = np.array([0.7, 1.9, 0.2])
+    inv = 2.5
+    q = np.broadcast_to(((sig + inv) * Q)[:, None, :], (ne, n, G)).copy()
+    fl = np.broadcast_to(Q, (2 * (nx + ny) * 3, G)).copy()
+    prob = Problem("c", 2, nx, ny, p, om, w, sig, q, fl, inv)
+    f = oracle.unpack(oracle.sweep(prob, opts=SIG), 2, nx, ny, p, opts=SIG)
+    ref = (sig * Q).sum(axis=1)[:, None]
+    assert np.abs(f["sphi"] - ref).max() < 1e-13 * ref.max()
+    assert np.abs(f["sJ"]).max() < 1e-13 * ref.max()
+
+
+def test_sigma_moments_leave_base_fields_unchanged():
+    prob = random_problem(12, 2, 3, 3, 2, 4, 2)
+    a = oracle.sweep(prob)
+    b = oracle.sweep(prob, opts=SIG)
+    assert np.array_equal(a, b[:a.size])
+
+
+# ------------------------------------------------------------------ NEXT-2
+def test_fixup_worked_examples():
+    """SPEC.md fixup examples (1-D p=1, equal weights) and two weighted 2-D cases."""
+    W = np.array([0.5, 0.5])
+    assert np.array_equal(oracle.fixup([1.0, 2.0], W), [1.0, 2.0])          # unchanged
+    assert np.allclose(oracle.fixup([-1.0, 3.0], W), [0.0, 2.0], atol=1e-15)  # average 1 kept
+    assert np.array_equal(oracle.fixup([-2.0, 1.0], W), [0.0, 0.0])         # non-positive average
+    W4 = np.full(4, 0.25)
+    assert np.allclose(oracle.fixup([-1.0, 1.0, 2.0, 2.0], W4), [0.0, 0.8, 1.6, 1.6], atol=1e-15)
+    wh = np.array([1.0, 4.0, 1.0]) / 6.0
+    W9 = np.outer(wh, wh).reshape(-1)
+    x = np.array([1.0, -0.5, 1.0, 2.0, 1.0, 2.0, -0.1, 3.0, 1.0])
+    y = oracle.fixup(x, W9)
+    assert (y >= 0).all() and y[1] == 0 and y[6] == 0
+    assert abs(W9 @ y - W9 @ x) < 1e-15 * abs(W9 @ x)
+    assert np.allclose(y[x > 0] / x[x > 0], (W9 @ x) / (W9 @ np.maximum(x, 0)), rtol=1e-15)
+
+
+def _negative_problem(dim, p, seed):
+    """Thick cells, a grazing direction set and steep inflow: the unfixed DG solution
+    goes negative somewhere (checked by the tests that use it)."""
+    nx, ny = (6, 1) if dim == 1 else (4, 4)
+    prob = random_problem(seed, dim, nx, ny, p, 6, 2, sigma_range=(5.0, 400.0), inv_c_dt=0.1)
+    prob.q[:] = 1e-3
+    prob.inflow[:] = 0.0
+    prob.inflow[: max(1, prob.inflow.shape[0] // 4)] = 50.0
+    return prob
+
+
+@pytest.mark.parametrize("dim,p", [(1, 2), (2, 1), (2, 2)])
+def test_fixup_sweep_equals_block_substitution(dim, p):
+    """psi with the fixup = element-by-element block substitution of the independently
+    assembled global system with the fixup applied per element (tests/dense_dg.py)."""
+    prob = _negative_problem(dim, p, 0)
+    neg = False
+    for d in range(prob.n_dir):
+        for g in range(prob.G):
+            plain = oracle.sweep_psi(prob, d, g)
+            neg |= bool((plain < -1e-12 * np.abs(plain).max()).any())
+            got = oracle.sweep_psi(prob, d, g, opts=FIX)
+            ref = sweep_blocks(prob, d, g, fixup=True)
+            assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (d, g)
+            assert (got >= 0).all()
+    assert neg, "the test problem must exercise the fixup"
+
+
+def test_fixup_is_identity_without_negatives():
+    """Constant solution (psi == Q > 0 everywhere): fixup on and off agree bit for bit."""
+    nx, ny, p, G = 4, 3, 2, 2
+    om, w = synth.product_set(2, 8)
+    sig = np.full((nx * ny, G), 3.0)
+    Q = np.array([1.0, 2.0])
+    q = np.broadcast_to(((sig + 1.0) * Q)[:, None, :], (nx * ny, 9, G)).copy()
+    fl = np.broadcast_to(Q, (2 * (nx + ny) * 3, G)).copy()
+    prob = Problem("c", 2, nx, ny, p, om, w, sig, q, fl, 1.0)
+    assert np.array_equal(oracle.sweep(prob), oracle.sweep(prob, opts=FIX))
