@@ -32,7 +32,13 @@
  *
  * Output packing (doubles), all gray = summed over every group of every rank:
  *   phi[N_el][n] | J[dim][N_el][n] | T[nT][N_el][n] | beta[N_bnode] | Jplus[N_bnode]
+ *   [ | sphi[N_el][n] | sJ[dim][N_el][n]    with SWEEP_SIGMA_MOMENTS ]
  *   nT = 1 (dim 1: T_xx) or 3 (dim 2: T_xx, T_xy, T_yy; T_zz = -T_xx - T_yy).
+ *   sphi = sum_g sigma_t,g phi_g and sJ = sum_g sigma_t,g J_g are the sigma-weighted
+ *   gray moments the gray low-order system takes from the sweep: the numerator of
+ *   sigma_E (eq:sigmaE) and the high-order part of the additive
+ *   multigroup correction sum_g (sigma_F - sigma_g) F_g (eq:additive_mg_correction,
+ *   PAPER.md:197-203, :247).  sigma_t excludes 1/(c dt).
  *
  * Every function returns an int status (SWEEP_OK = 0) and never aborts or
  * throws across the ABI; sweep_last_error gives the message of the last
@@ -65,6 +71,13 @@ enum {
                                     (e.g. +-Omega_z) once with the summed weight; exact (reading R20) */
 #define SWEEP_DETERMINISTIC 2u   /* accepted for API compatibility: every reduction already runs in a
                                     fixed order, so results are bitwise repeatable in all modes */
+#define SWEEP_SIGMA_MOMENTS 4u   /* also return sphi, sJ (see the output packing above) */
+#define SWEEP_FIXUP 8u           /* zero-and-scale negative flux fixup inside the sweep (PAPER.md:987,
+                                    :1321): after every element solve, negative nodal values are set
+                                    to 0 and the others scaled to keep the element integral
+                                    sum_k W_k psi_k (W_k the lumped GLL mass); a non-positive integral
+                                    zeroes the element.  The downwind elements see the fixed values.
+                                    Nonlinear: no longer the solution of one linear system. */
 
 typedef struct sweep_handle sweep_handle;   /* opaque, owned by the library */
 
@@ -82,7 +95,7 @@ typedef struct {
     int device;              /* CUDA device ordinal */
     int nranks, rank;        /* nranks = 1: no collective; > 1: NCCL all-reduce of the gray output */
     const void *nccl_id;     /* 128-byte ncclUniqueId created by rank 0 and broadcast (nranks > 1), else NULL */
-    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC */
+    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC | SWEEP_SIGMA_MOMENTS | SWEEP_FIXUP */
 } sweep_desc;
 
 /* Validate the description, fold/sort directions into sweep quadrants,
@@ -92,9 +105,9 @@ typedef struct {
  * *out receives the handle, or NULL on failure. */
 int sweep_setup(const sweep_desc *desc, sweep_handle **out);
 
-/* Offsets (in doubles) of phi, J, T, beta, Jplus inside the packed output,
- * and its total length. */
-int sweep_layout(const sweep_handle *h, size_t off[5], size_t *total_doubles);
+/* Offsets (in doubles) of phi, J, T, beta, Jplus, sphi, sJ inside the packed
+ * output, and its total length (off[5] = off[6] = total without SWEEP_SIGMA_MOMENTS). */
+int sweep_layout(const sweep_handle *h, size_t off[7], size_t *total_doubles);
 
 /* One sweep + fused closures, enqueued asynchronously on cuda_stream
  * (a cudaStream_t; NULL = legacy default stream).  Device pointers, borrowed,

@@ -9,10 +9,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsweep.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("sweep_kernels.cu", "sweep_host.cpp")]
-HEADERS = [os.path.join(CSRC, "sweep_internal.h"), os.path.join(ROOT, "include", "sweep.h")]
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC,-O2", "-shared", "-ldl"]
+# device code is split over translation units that compile in parallel
+# (k2d_*.cu instantiate the 2-D kernel templates of sweep_device.cuh)
+SOURCES = [os.path.join(CSRC, f) for f in ("k2d_p2.cu", "k2d_opt_p2.cu", "k2d_p1.cu", "k2d_opt_p1.cu",
+                                           "k_common.cu", "sweep_host.cpp")]
+HEADERS = [os.path.join(CSRC, "sweep_internal.h"), os.path.join(CSRC, "sweep_device.cuh"),
+           os.path.join(ROOT, "include", "sweep.h")]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMPILE_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2"]
+NVCC_FLAGS = [*COMPILE_FLAGS, "-shared", "-ldl"]    # single-command form (experiment builds)
 
 
 def nvcc() -> str:
@@ -29,17 +34,43 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def compile_objects(out_dir: str, extra=(), verbose: bool = False) -> list:
+    """nvcc -c every source in parallel; returns the object paths."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(out_dir, exist_ok=True)
+
+    def one(src):
+        obj = os.path.join(out_dir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *COMPILE_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stderr.write(r.stderr)
+        if r.returncode:
+            raise subprocess.CalledProcessError(r.returncode, cmd)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        return list(ex.map(one, SOURCES))
+
+
+def link(objs: list, out: str) -> None:
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-ldl"])
+
+
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) -> str:
+    if out == LIB and not extra and not force and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    tag = f"{os.getpid()}_{abs(hash(tuple(extra))) % 10**8}"
+    objs = compile_objects(os.path.join(ROOT, "build", "obj_" + tag), extra, verbose)
+    tmp = out + f".tmp{os.getpid()}"
+    link(objs, tmp)
+    os.replace(tmp, out)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(os.path.dirname(objs[0]))
+    return out
 
 
 if __name__ == "__main__":

@@ -1,0 +1,160 @@
+// k_common.cu — the 1-D sweep kernels, the slab reduction, the FP64 probe and the
+// launch dispatch over the 2-D translation units (k2d_*.cu).
+#include "sweep_device.cuh"
+
+namespace sweepk {
+
+// ------------------------------------------------------------------ finalize
+__global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, size_t n, double* __restrict__ out,
+                                int* err) {
+    bool bad = false;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < n_slabs; ++s) acc += __ldcs(slabs + (size_t)s * n + i);
+        out[i] = acc;
+        bad |= !(fabs(acc) < 1.0e300);
+    }
+    if (bad) atomicOr(err, 2);
+}
+
+// ------------------------------------------------------------------ launchers
+template <int P, int OPT>
+static const void* pick1d_lg(int log2gb) {
+    switch (log2gb) {
+        case 0: return (const void*)sweep1d_kernel<P, 0, OPT>;
+        case 1: return (const void*)sweep1d_kernel<P, 1, OPT>;
+        case 2: return (const void*)sweep1d_kernel<P, 2, OPT>;
+        case 3: return (const void*)sweep1d_kernel<P, 3, OPT>;
+        case 4: return (const void*)sweep1d_kernel<P, 4, OPT>;
+        default: return (const void*)sweep1d_kernel<P, 5, OPT>;
+    }
+}
+template <int P>
+static const void* pick1d(int log2gb, int opt) {
+    switch (opt) {
+        case 0: return pick1d_lg<P, 0>(log2gb);
+        case 1: return pick1d_lg<P, 1>(log2gb);
+        case 2: return pick1d_lg<P, 2>(log2gb);
+        default: return pick1d_lg<P, 3>(log2gb);
+    }
+}
+
+static const void* pick2d(int p, int log2lg, int k, int opt) {
+    if (opt == 0) return (p == 2) ? pick2d_p2(log2lg, k) : pick2d_p1(log2lg, k);
+    return (p == 2) ? pick2d_opt_p2(log2lg, k, opt) : pick2d_opt_p1(log2lg, k, opt);
+}
+
+int upload_modal(const ModalConsts& mc) {
+    int e = (int)cudaMemcpyToSymbol(cM, &mc, sizeof(ModalConsts));
+    if (!e) e = upload_modal_p1(mc);
+    if (!e) e = upload_modal_p2(mc);
+    if (!e) e = upload_modal_opt_p1(mc);
+    if (!e) e = upload_modal_opt_p2(mc);
+    return e;
+}
+
+int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
+    const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k, opt), NQ = nq_of(p), NN = (p + 1) * (p + 1);
+    const int CT = C * T;
+    const int NL = dset * gbk / k;  // threads per CTA
+    const int nfo = (opt & OPT_SIGMA) ? 9 : 6;
+    const int s2 = (opt & OPT_SIGMA) ? CT * (dset * NQ + 1) : 0;
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + CT * nfo * NQ + 81 +
+            s2) *
+           (int)sizeof(double);
+}
+int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
+int sweep2d_cols_per_chunk(int p, int k, int opt) { return cols_per_chunk(p, k, opt); }
+
+int sweep2d_occupancy(int p, int log2lg, int k, int opt, int block, size_t smem, int* blocks_per_sm) {
+    const void* f = pick2d(p, log2lg, k, opt);
+    if (!f) return (int)cudaErrorInvalidDeviceFunction;
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+}
+
+int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, int grid, int block, size_t smem,
+                   void* stream) {
+    const void* f = pick2d(p, log2lg, k, opt);
+    if (!f) return (int)cudaErrorInvalidDeviceFunction;
+    void* args[] = {(void*)&prm};
+    return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
+}
+
+int launch_sweep1d(int p, int log2gb, int opt, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream) {
+    const void* f = (p == 2) ? pick1d<2>(log2gb, opt) : pick1d<1>(log2gb, opt);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+    }
+    void* args[] = {(void*)&prm};
+    return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
+}
+
+int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream) {
+    const int block = 256;
+    size_t want = (out_size + block - 1) / block;
+    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+    if (grid < 1) grid = 1;
+    finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, out_size, out, err);
+    return (int)cudaGetLastError();
+}
+
+const char* cuda_err_string(int e) { return cudaGetErrorString((cudaError_t)e); }
+
+// FP64 pipe probe: 8 independent DFMA chains per thread, enough warps per SM to
+// hide the DFMA latency.  flops = 2 * 8 * iters per thread.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters, double b, double c) {
+    double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+           a7 = a0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fma(a0, b, c);
+            a1 = fma(a1, b, c);
+            a2 = fma(a2, b, c);
+            a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c);
+            a5 = fma(a5, b, c);
+            a6 = fma(a6, b, c);
+            a7 = fma(a7, b, c);
+        }
+    }
+    const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == 1.2345) sink[threadIdx.x] = r;  // keep the chains alive
+}
+
+int fp64_probe(int device, double* tflops) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e) return (int)e;
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    double* sink = nullptr;
+    if ((e = cudaMalloc(&sink, 256 * sizeof(double)))) return (int)e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int iters = 4096, blocks = nsm * 8, threads = 256;
+    fp64_probe_kernel<<<blocks, threads>>>(sink, 64, 0.999999, 1e-7);  // warm up
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        fp64_probe_kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-7);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e) return (int)e;
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return 0;
+}
+
+}  // namespace sweepk

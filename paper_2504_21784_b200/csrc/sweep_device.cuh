@@ -1,4 +1,8 @@
-// sweep_kernels.cu — sm_100a kernels of the fused DG S_N sweep + gray SM closures.
+#pragma once
+// sweep_device.cuh — sm_100a device code of the fused DG S_N sweep + gray SM closures
+// (kernel templates and helpers).  Instantiated by the k_*.cu translation units,
+// which are compiled in parallel; each unit has its own copy of the constant bank
+// cM (upload_modal writes all of them).
 //
 // Method: for each direction d and group g the lumped upwind-DG
 // element system (eq:dgsn_transport PAPER.md:332-336, GLL lumping :654) is
@@ -34,19 +38,21 @@
 
 namespace sweepk {
 
-__constant__ ModalConsts cM;
+static __constant__ ModalConsts cM;  // per translation unit
 
 #ifdef SWEEP_TRACE
 // debug timeline (trace builds only): per task [start, end, waited ns, sm id]
-__device__ long long g_trace[1 << 18][8];
+static __device__ long long g_trace[1 << 18][8];
 __device__ __forceinline__ long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#ifdef SWEEP_TRACE_OWNER
 extern "C" int sweep_debug_trace(long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 8 * (size_t)n);
 }
+#endif
 #endif
 
 #define FULLMASK 0xffffffffu
@@ -136,7 +142,9 @@ struct LaneP2 {
     double I01s, I10s, I11s, I12s;
 };
 
-__device__ __forceinline__ LaneP2 make_lane_p2(double cx, double cy) {
+// kap: 1/(c dt) folded into the mode shifts when the staged opacity is sigma_t
+// (sigma-weighted moments need sigma_t itself); 0 when the staged value is sigma~
+__device__ __forceinline__ LaneP2 make_lane_p2(double cx, double cy, double kap = 0.0) {
     LaneP2 L;
     const double l0 = cM.lam0, mu = cM.mu, nu = cM.nu;
     L.lx0 = 6.0 * cx * cM.W0[0];
@@ -145,10 +153,10 @@ __device__ __forceinline__ LaneP2 make_lane_p2(double cx, double cy) {
     L.ly0 = 6.0 * cy * cM.W0[0];
     L.ly1r = 6.0 * cy * cM.W1re[0];
     L.ly1i = 6.0 * cy * cM.W1im[0];
-    L.A00 = (cx + cy) * l0;
-    L.A01 = cx * l0 + cy * mu;
-    L.A10 = cx * mu + cy * l0;
-    L.A11 = (cx + cy) * mu;
+    L.A00 = (cx + cy) * l0 + kap;
+    L.A01 = (cx * l0 + cy * mu) + kap;
+    L.A10 = (cx * mu + cy * l0) + kap;
+    L.A11 = (cx + cy) * mu + kap;
     L.I01 = cy * nu;
     L.I10 = cx * nu;
     L.I11 = (cx + cy) * nu;
@@ -159,6 +167,8 @@ __device__ __forceinline__ LaneP2 make_lane_p2(double cx, double cy) {
     L.I12s = L.I12 * L.I12;
     return L;
 }
+
+__device__ __forceinline__ void traces_p2(const double (&u)[9], double (&txo)[3], double (&tyo)[3]);
 
 // modal element solve: u = (sigma~ + cx lam_a + cy lam_b)^-1 (q^ + lifts), and the
 // outflow traces in modal form (x+ face: y-modal, y+ face: x-modal).
@@ -201,7 +211,11 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     u[6] = (r11i * e11 - r11r * L.I11) * i11;
     u[7] = (r12r * e11 + r12i * L.I12) * i12;
     u[8] = (r12i * e11 - r12r * L.I12) * i12;
+    traces_p2(u, txo, tyo);
+}
 
+// outflow traces of a modal element solution: x+ face (y-modal), y+ face (x-modal)
+__device__ __forceinline__ void traces_p2(const double (&u)[9], double (&txo)[3], double (&tyo)[3]) {
     const double v0 = cM.V0[2], vr = cM.V1re[2], vi = cM.V1im[2], vr2 = cM.V1re2x, vi2 = cM.V1im2x;
     const double sr = u[5] + u[7], dr = u[5] - u[7];
     const double si = u[6] + u[8], di = u[6] - u[8];
@@ -238,17 +252,67 @@ __device__ __forceinline__ void modal_forward(const double (&q)[9], double (&qh)
     qh[8] = ri - ir;
 }
 
+// ---- zero-and-scale negative flux fixup:
+// negative nodal values -> 0, the rest scaled so the element integral sum_k W_k psi_k
+// is kept; a non-positive integral zeroes the element.  W_k = w^_a w^_b (the element's
+// h factors cancel); the GLL weights are mirror symmetric, so sweep-coordinate node
+// order needs no remapping.
+template <int N>
+__device__ __forceinline__ bool fixup_nodal(double (&x)[N], const double (&W)[N]) {
+    bool neg = false;
+#pragma unroll
+    for (int k = 0; k < N; ++k) neg |= x[k] < 0.0;
+    if (!neg) return false;
+    double total = 0.0, pos = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        total += W[k] * x[k];
+        if (x[k] > 0.0) pos += W[k] * x[k];
+    }
+    if (total <= 0.0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) x[k] = 0.0;
+    } else {
+        const double scale = total / pos;
+#pragma unroll
+        for (int k = 0; k < N; ++k) x[k] = (x[k] > 0.0) ? x[k] * scale : 0.0;
+    }
+    return true;
+}
+// p = 2, modal u: nodal values (V (x) V) u, fixup, back to modal (W (x) W)
+__device__ __forceinline__ bool fixup_p2(double (&u)[9]) {
+    double x[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < 9; ++m) acc = fma(cM.bck[k][m], u[m], acc);
+        x[k] = acc;
+    }
+    constexpr double w0 = 1.0 / 6.0, w1 = 2.0 / 3.0;
+    const double W[9] = {w0 * w0, w1 * w0, w0 * w0, w0 * w1, w1 * w1, w0 * w1, w0 * w0, w1 * w0, w0 * w0};
+    if (!fixup_nodal<9>(x, W)) return false;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc = fma(cM.fwd[m][k], x[k], acc);
+        u[m] = acc;
+    }
+    return true;
+}
+
 // ------------------------------------------------------------------ 2-D, p = 1
 // closed-form inverse of a0 I + cx Jx + cy Jy (Jx^2 = Jy^2 = -I, K = Jx Jy):
 // (a0 - cx Jx - cy Jy)(al - be K) / (al^2 - be^2), al = a0^2 + cx^2 + cy^2, be = -2 cx cy.
 struct LaneP1 {
     double cx, cy, cxy, sq, be, be2, lx, ly;
 };
-__device__ __forceinline__ LaneP1 make_lane_p1(double cx, double cy) {
+__device__ __forceinline__ LaneP1 make_lane_p1(double cx, double cy, double kap = 0.0) {
     LaneP1 L;
     L.cx = cx;
     L.cy = cy;
-    L.cxy = cx + cy;
+    L.cxy = (cx + cy) + kap;
     L.sq = cx * cx + cy * cy;
     L.be = -2.0 * cx * cy;
     L.be2 = L.be * L.be;
@@ -289,7 +353,9 @@ __host__ __device__ constexpr int rows_per_strip(int P, int K) { return K >= 4 ?
 #ifndef SWEEP_COLS_K4
 #define SWEEP_COLS_K4 8
 #endif
-__host__ __device__ constexpr int cols_per_chunk(int P, int K) { return K >= 4 ? SWEEP_COLS_K4 : 4; }
+__host__ __device__ constexpr int cols_per_chunk(int P, int K, int OPT = 0) {
+    return K >= 4 ? ((OPT & OPT_SIGMA) ? 4 : SWEEP_COLS_K4) : 4;  // sigma moments: a second S buffer, half the chunk
+}
 // (K = 2: T = 4 rows, C = 4 columns -> 16 elements per chunk, like K = 4)
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
 
@@ -376,8 +442,12 @@ __device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc,
 //      zeroed staging and are never written out);
 //   C  direction sums with the moment / boundary weights, back to nodal values,
 //      written to this stream's slab.
-template <int P, int LOG2LG, int K>
+// OPT bits (compile time): OPT_SIGMA appends sum_g sigma_g (phi, J) (NEXT-1), OPT_FIXUP
+// applies the zero-and-scale fixup to every element solve (NEXT-2).
+template <int P, int LOG2LG, int K, int OPT>
 __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sweep2DParams prm) {
+    constexpr bool SIG = (OPT & OPT_SIGMA) != 0;
+    constexpr bool FIX = (OPT & OPT_FIXUP) != 0;
     constexpr int NP1 = P + 1;
     constexpr int NN = NP1 * NP1;
     constexpr int NQ = nq_of(P);
@@ -385,7 +455,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
     constexpr int LG = 1 << LOG2LG;
     constexpr int GBK = LG * K;
     constexpr int T = rows_per_strip(P, K);
-    constexpr int C = cols_per_chunk(P, K);
+    constexpr int C = cols_per_chunk(P, K, OPT);
     constexpr int CT = C * T;
     constexpr int NFIELD = 14;  // 6 moments + (beta, J+) x 4 faces
 
@@ -501,8 +571,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
         // phase-C weights of this stream's directions: [dd][14]
         double* coefS = S + (size_t)CT * SEL;
         double* ypre = coefS + dset * NFIELD;  // [K*NT][NL] next-column trace prefetch
-        double* Mbuf = ypre + K * NT * NL;     // [CT][6][NQ] direction sums (phase C stage 1, p = 2)
-        double* bckS = Mbuf + CT * 6 * NQ;     // [9][9] modal -> nodal (p = 2)
+        constexpr int NFO = SIG ? 9 : 6;       // node fields: 6 moments (+ sigma phi, sigma Jx, sigma Jy)
+        double* Mbuf = ypre + K * NT * NL;     // [CT][NFO][NQ] direction sums (phase C stage 1, p = 2)
+        double* bckS = Mbuf + CT * NFO * NQ;   // [9][9] modal -> nodal (p = 2)
+        double* S2 = bckS + 81;                // SIG: [CT][SEL] sigma-weighted group sums
+        const size_t sig_off = 6 * nodes + 2 * (size_t)prm.nbnode;  // SIG: sigma phi | sigma J
         // (compile-time constant-bank indices only: ptxas hoists constant loads out of
         // the task loop for every thread, and a thread-dependent index past the end of
         // the constant bank is a fatal illegal instruction)
@@ -581,8 +654,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                     qv[kk] = on ? qs[((size_t)el * NN + a + NP1 * b) * GBK + gg] : 0.0;
                 }
                 if (on) {
-                    st = ss[el * GBK + gg] + prm.inv_c_dt;
-                    if (bad_sigma(st)) atomicOr(prm.err, 1);
+                    // SIG keeps sigma_t itself staged (1/(c dt) is folded into the lane's
+                    // mode shifts); otherwise sigma~ = sigma_t + 1/(c dt)
+                    const double sg = ss[el * GBK + gg];
+                    if (bad_sigma(sg + prm.inv_c_dt)) atomicOr(prm.err, 1);
+                    st = SIG ? sg : sg + prm.inv_c_dt;
                 }
                 ss[el * GBK + gg] = st;
                 if constexpr (P == 2) {
@@ -627,8 +703,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             if (bulk && c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);  // prefetch the next chunk
             using LaneC = typename std::conditional<P == 2, LaneP2, LaneP1>::type;
             LaneC L;
-            if constexpr (P == 2) L = make_lane_p2(cx, cy);
-            else L = make_lane_p1(cx, cy);
+            const double kap = SIG ? prm.inv_c_dt : 0.0;
+            if constexpr (P == 2) L = make_lane_p2(cx, cy, kap);
+            else L = make_lane_p1(cx, cy, kap);
             const int nxp = prm.nx_pad;
             const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)(K * NT) * NL;
             double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)(K * NT) * NL;
@@ -729,7 +806,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
                     const int el = col * T + r;
-                    double us[NQ];
+                    // us: group sum of the modal solution; SIG also the sigma-weighted sum
+                    double us[SIG ? 2 * NQ : NQ];
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         double qh[NQ], u[NQ], txo[NT], tyo[NT];
@@ -738,6 +816,19 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         const double st = ss[el * GBK + gl + k * LG];
                         if constexpr (P == 2) solve_p2(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
                         else solve_p1(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
+                        if constexpr (FIX) {
+                            if constexpr (P == 2) {
+                                if (fixup_p2(u)) traces_p2(u, txo, tyo);
+                            } else {
+                                const double W4[4] = {0.25, 0.25, 0.25, 0.25};
+                                if (fixup_nodal<4>(u, W4)) {
+                                    txo[0] = u[1];
+                                    txo[1] = u[3];
+                                    tyo[0] = u[2];
+                                    tyo[1] = u[3];
+                                }
+                            }
+                        }
 #pragma unroll
                         for (int t = 0; t < NT; ++t) {
                             tx[k][r][t] = txo[t];
@@ -745,14 +836,27 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         }
 #pragma unroll
                         for (int m = 0; m < NQ; ++m) us[m] = (k == 0) ? u[m] : us[m] + u[m];
+                        if constexpr (SIG) {
+#pragma unroll
+                            for (int m = 0; m < NQ; ++m) us[NQ + m] = (k == 0) ? st * u[m] : fma(st, u[m], us[NQ + m]);
+                        }
                     }
                     double* Sd = S + (size_t)el * SEL + dl * NQ;
-                    auto sink = [&](int idx, double val) { Sd[idx] = val; };
+                    if constexpr (SIG) {
+                        double* Sd2 = S2 + (size_t)el * SEL + dl * NQ;
+                        auto sink = [&](int idx, double val) {
+                            if (idx < NQ) Sd[idx] = val;
+                            else Sd2[idx - NQ] = val;
+                        };
+                        ReduceScatter<2 * NQ, LG / 2>::run(us, lane, 0, 2 * NQ, sink);
+                    } else {
+                        auto sink = [&](int idx, double val) { Sd[idx] = val; };
 #ifndef SWEEP_ABL_NORED
-                    ReduceScatter<NQ, LG / 2>::run(us, lane, 0, NQ, sink);
+                        ReduceScatter<NQ, LG / 2>::run(us, lane, 0, NQ, sink);
 #else
-                    if (lane == 0) Sd[0] = us[0] + us[1] + us[2] + us[3] + us[NQ - 1];
+                        if (lane == 0) Sd[0] = us[0] + us[1] + us[2] + us[3] + us[NQ - 1];
 #endif
+                    }
                 }
 #ifdef SWEEP_ABL_NOYTR
                 if (false) {
@@ -795,11 +899,16 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                     const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
                     dst[a + NP1 * b] = v;
                 };
-                for (int o = tid; o < CT * 6 * NQ; o += NL) {
+                // field f < 6: the moments from S; SIG f = 6, 7, 8: sigma phi, sigma Jx,
+                // sigma Jy from S2 with the weights of phi, Jx, Jy
+                auto field_dst = [&](int f) -> double* {
+                    return slab + ((f < 6) ? (size_t)f * nodes : sig_off + (size_t)(f - 6) * nodes);
+                };
+                for (int o = tid; o < CT * NFO * NQ; o += NL) {
                     const int m = o % NQ, rest = o / NQ;
-                    const int f = rest % 6, el = rest / 6;
-                    const double* Sp = S + (size_t)el * SEL + m;
-                    const double* cf = coefS + f;
+                    const int f = rest % NFO, el = rest / NFO;
+                    const double* Sp = ((f < 6) ? S : S2) + (size_t)el * SEL + m;
+                    const double* cf = coefS + ((f < 6) ? f : f - 6);
                     double a0 = 0.0, a1 = 0.0;
                     int dd = 0;
                     for (; dd + 1 < sd.nd; dd += 2) {
@@ -815,7 +924,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         if (col < cols && r < rows) {
                             const int ip = i0 + col, jp = j0 + r;
                             const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                            node_store(slab + (size_t)f * nodes + ((size_t)i + (size_t)nx * j) * NN, m, acc);
+                            node_store(field_dst(f) + ((size_t)i + (size_t)nx * j) * NN, m, acc);
                         }
                     }
                 }
@@ -871,9 +980,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                 }
                 if constexpr (P == 2) {
                     __syncthreads();
-                    for (int o = tid; o < CT * 6 * NN; o += NL) {
+                    for (int o = tid; o < CT * NFO * NN; o += NL) {
                         const int kk = o % NN, rest = o / NN;
-                        const int f = rest % 6, el = rest / 6;
+                        const int f = rest % NFO, el = rest / NFO;
                         const int col = el / T, r = el - col * T;
                         if (col >= cols || r >= rows) continue;
                         const double* Mp = Mbuf + rest * NQ;
@@ -883,7 +992,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         for (int m = 0; m < 9; ++m) v = fma(bk[m], Mp[m], v);
                         const int ip = i0 + col, jp = j0 + r;
                         const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                        node_store(slab + (size_t)f * nodes + ((size_t)i + (size_t)nx * j) * NN, kk, v);
+                        node_store(field_dst(f) + ((size_t)i + (size_t)nx * j) * NN, kk, v);
                     }
                 }
             }
@@ -945,8 +1054,10 @@ __device__ __forceinline__ void solve1d(double c, double st, const double (&q)[P
     }
 }
 
-template <int P, int LOG2GB>
+template <int P, int LOG2GB, int OPT>
 __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) {
+    constexpr bool SIG = (OPT & OPT_SIGMA) != 0;  // + sigma phi, sigma J (NEXT-1)
+    constexpr bool FIX = (OPT & OPT_FIXUP) != 0;  // zero-and-scale fixup (NEXT-2); host runs one segment
     constexpr int NP1 = P + 1;
     constexpr int GB = 1 << LOG2GB;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -976,13 +1087,15 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
     double* slab = prm.slabs + (size_t)blockIdx.x * prm.out_size;
     const size_t nodes = prm.nodes;
 
-    auto load = [&](int ip, double& st, double (&q)[NP1]) {
+    auto load = [&](int ip, double& st, double (&q)[NP1], double& sg) {
         const int i = fx ? nx - 1 - ip : ip;
         st = 1.0;
+        sg = 0.0;
 #pragma unroll
         for (int a = 0; a < NP1; ++a) q[a] = 0.0;
         if (g_on) {
-            st = prm.sigma[(size_t)i * G + g] + prm.inv_c_dt;
+            sg = prm.sigma[(size_t)i * G + g];
+            st = sg + prm.inv_c_dt;
             if (bad_sigma(st)) atomicOr(prm.err, 1);
 #pragma unroll
             for (int aq = 0; aq < NP1; ++aq) {
@@ -993,10 +1106,12 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
     };
 
     // phase 1: compose the affine maps of this segment
+    // (with the fixup the chain is not affine: the host runs a single segment, whose
+    // inflow is the boundary value, and this composition is skipped)
     double Tm = 1.0, Sm = 0.0;
-    for (int ip = e_begin; ip < e_end; ++ip) {
-        double st, q[NP1], psi[NP1], ta, sa;
-        load(ip, st, q);
+    for (int ip = e_begin; ip < (FIX ? e_begin : e_end); ++ip) {
+        double st, q[NP1], psi[NP1], ta, sa, sg;
+        load(ip, st, q, sg);
         solve1d<P>(c, st, q, 0.0, psi, ta, sa);
         Sm = fma(ta, Sm, sa);
         Tm = ta * Tm;
@@ -1017,26 +1132,43 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
     // phase 3: final sweep of the segment + moments
     double up = IN[w * 32 + lane];
     for (int ip = e_begin; ip < e_end; ++ip) {
-        double st, q[NP1], psi[NP1], ta, sa;
-        load(ip, st, q);
+        double st, q[NP1], psi[NP1], ta, sa, sg;
+        load(ip, st, q, sg);
         solve1d<P>(c, st, q, up, psi, ta, sa);
+        if constexpr (FIX) {
+            double W[NP1];
+            if constexpr (P == 1) {
+                W[0] = W[1] = 0.5;
+            } else {
+                W[0] = W[2] = 1.0 / 6.0;
+                W[1] = 2.0 / 3.0;
+            }
+            fixup_nodal<NP1>(psi, W);
+        }
         up = psi[P];
         const int i = fx ? nx - 1 - ip : ip;
-        double v[3 * NP1];
+        constexpr int NV = (SIG ? 5 : 3) * NP1;  // phi, J, Txx (+ sigma phi, sigma J)
+        double v[NV];
 #pragma unroll
         for (int aq = 0; aq < NP1; ++aq) {
             v[0 * NP1 + aq] = cm0 * psi[aq];
             v[1 * NP1 + aq] = cm1 * psi[aq];
             v[2 * NP1 + aq] = cm2 * psi[aq];
+            if constexpr (SIG) {
+                v[3 * NP1 + aq] = sg * v[0 * NP1 + aq];
+                v[4 * NP1 + aq] = sg * v[1 * NP1 + aq];
+            }
         }
+        const size_t sig_off = 3 * nodes + 4;  // after phi, J, Txx, beta[2], J+[2]
         auto sink = [&](int idx, double val) {
-            if (idx < 3 * NP1) {
+            if (idx < NV) {
                 const int m = idx / NP1, aq = idx - m * NP1;
                 const int a = fx ? P - aq : aq;
-                slab[(size_t)m * nodes + (size_t)i * NP1 + a] = val;
+                const size_t base = (m < 3) ? (size_t)m * nodes : sig_off + (size_t)(m - 3) * nodes;
+                slab[base + (size_t)i * NP1 + a] = val;
             }
         };
-        ReduceScatter<3 * NP1, 16>::run(v, lane, 0, 3 * NP1, sink);
+        ReduceScatter<NV, 16>::run(v, lane, 0, NV, sink);
         if (i == 0 || i == nx - 1) {  // warp-uniform
             // boundary closures at x = 0 (node a = 0) and x = lx (node a = P)
             const double p0 = psi[fx ? P : 0], p1 = psi[fx ? 0 : P];
@@ -1055,155 +1187,6 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
             ReduceScatter<4, 16>::run(bv, lane, 0, 4, bsink);
         }
     }
-}
-
-// ------------------------------------------------------------------ finalize
-__global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, size_t n, double* __restrict__ out,
-                                int* err) {
-    bool bad = false;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int s = 0; s < n_slabs; ++s) acc += __ldcs(slabs + (size_t)s * n + i);
-        out[i] = acc;
-        bad |= !(fabs(acc) < 1.0e300);
-    }
-    if (bad) atomicOr(err, 2);
-}
-
-// ------------------------------------------------------------------ launchers
-template <int P, int K>
-static const void* pick2d_k(int log2lg) {
-    switch (log2lg) {
-        case 0: return (const void*)sweep2d_kernel<P, 0, K>;
-        case 1: return (const void*)sweep2d_kernel<P, 1, K>;
-        case 2: return (const void*)sweep2d_kernel<P, 2, K>;
-        case 3: return (const void*)sweep2d_kernel<P, 3, K>;
-        case 4: return (const void*)sweep2d_kernel<P, 4, K>;
-        default: return (const void*)sweep2d_kernel<P, 5, K>;
-    }
-}
-static const void* pick2d(int p, int log2lg, int k) {
-    if (p == 2) return (k == 4) ? pick2d_k<2, 4>(log2lg) : (k == 2) ? pick2d_k<2, 2>(log2lg) : pick2d_k<2, 1>(log2lg);
-    return (k == 4) ? pick2d_k<1, 4>(log2lg) : (k == 2) ? pick2d_k<1, 2>(log2lg) : pick2d_k<1, 1>(log2lg);
-}
-template <int P>
-static const void* pick1d() {
-    return (const void*)sweep1d_kernel<P, 0>;
-}
-
-int upload_modal(const ModalConsts& mc) { return (int)cudaMemcpyToSymbol(cM, &mc, sizeof(ModalConsts)); }
-
-int sweep2d_smem_bytes(int p, int k, int gbk, int dset) {
-    const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k), NQ = nq_of(p), NN = (p + 1) * (p + 1);
-    const int CT = C * T;
-    const int NL = dset * gbk / k;  // threads per CTA
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + CT * 6 * NQ + 81) *
-           (int)sizeof(double);
-}
-int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
-int sweep2d_cols_per_chunk(int p, int k) { return cols_per_chunk(p, k); }
-
-int sweep2d_occupancy(int p, int log2lg, int k, int block, size_t smem, int* blocks_per_sm) {
-    const void* f = pick2d(p, log2lg, k);
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
-}
-
-int launch_sweep2d(int p, int log2lg, int k, const Sweep2DParams& prm, int grid, int block, size_t smem,
-                   void* stream) {
-    const void* f = pick2d(p, log2lg, k);
-    void* args[] = {(void*)&prm};
-    return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
-}
-
-int launch_sweep1d(int p, int log2gb, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream) {
-    const void* f;
-    switch (p * 8 + log2gb) {
-        case 8 + 0: f = (const void*)sweep1d_kernel<1, 0>; break;
-        case 8 + 1: f = (const void*)sweep1d_kernel<1, 1>; break;
-        case 8 + 2: f = (const void*)sweep1d_kernel<1, 2>; break;
-        case 8 + 3: f = (const void*)sweep1d_kernel<1, 3>; break;
-        case 8 + 4: f = (const void*)sweep1d_kernel<1, 4>; break;
-        case 8 + 5: f = (const void*)sweep1d_kernel<1, 5>; break;
-        case 16 + 0: f = (const void*)sweep1d_kernel<2, 0>; break;
-        case 16 + 1: f = (const void*)sweep1d_kernel<2, 1>; break;
-        case 16 + 2: f = (const void*)sweep1d_kernel<2, 2>; break;
-        case 16 + 3: f = (const void*)sweep1d_kernel<2, 3>; break;
-        case 16 + 4: f = (const void*)sweep1d_kernel<2, 4>; break;
-        default: f = (const void*)sweep1d_kernel<2, 5>; break;
-    }
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-    }
-    void* args[] = {(void*)&prm};
-    return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
-}
-
-int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream) {
-    const int block = 256;
-    size_t want = (out_size + block - 1) / block;
-    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
-    if (grid < 1) grid = 1;
-    finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, out_size, out, err);
-    return (int)cudaGetLastError();
-}
-
-const char* cuda_err_string(int e) { return cudaGetErrorString((cudaError_t)e); }
-
-// FP64 pipe probe: 8 independent DFMA chains per thread, enough warps per SM to
-// hide the DFMA latency.  flops = 2 * 8 * iters per thread.
-__global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters, double b, double c) {
-    double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
-           a7 = a0 + 7;
-    for (int i = 0; i < iters; ++i) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            a0 = fma(a0, b, c);
-            a1 = fma(a1, b, c);
-            a2 = fma(a2, b, c);
-            a3 = fma(a3, b, c);
-            a4 = fma(a4, b, c);
-            a5 = fma(a5, b, c);
-            a6 = fma(a6, b, c);
-            a7 = fma(a7, b, c);
-        }
-    }
-    const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
-    if (r == 1.2345) sink[threadIdx.x] = r;  // keep the chains alive
-}
-
-int fp64_probe(int device, double* tflops) {
-    cudaError_t e = cudaSetDevice(device);
-    if (e) return (int)e;
-    int nsm = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    double* sink = nullptr;
-    if ((e = cudaMalloc(&sink, 256 * sizeof(double)))) return (int)e;
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    const int iters = 4096, blocks = nsm * 8, threads = 256;
-    fp64_probe_kernel<<<blocks, threads>>>(sink, 64, 0.999999, 1e-7);  // warm up
-    float best = 1e30f;
-    for (int rep = 0; rep < 3; ++rep) {
-        cudaEventRecord(a);
-        fp64_probe_kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-7);
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        if (ms < best) best = ms;
-    }
-    e = cudaGetLastError();
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(sink);
-    if (e) return (int)e;
-    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
-    *tflops = flops / (best * 1e-3) / 1e12;
-    return 0;
 }
 
 }  // namespace sweepk

@@ -90,7 +90,8 @@ struct sweep_handle {
     int dim, nx, ny, p, n, np1, nbnode, G, device, nranks, rank;
     double lx, ly, hx, hy;
     unsigned flags;
-    size_t nodes, out_size, off[5];
+    size_t nodes, out_size, off[7];
+    int opt = 0;  // sweepk::OPT_* bits from the flags
     int n_dir_in, n_dir_eff;
     // schedule
     int log2gb, gb, kpl, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
@@ -336,6 +337,14 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     h->off[3] = h->nodes * (1 + D.dim + nT);
     h->off[4] = h->off[3] + h->nbnode;
     h->out_size = h->off[4] + h->nbnode;
+    h->opt = ((D.flags & SWEEP_SIGMA_MOMENTS) ? sweepk::OPT_SIGMA : 0) | ((D.flags & SWEEP_FIXUP) ? sweepk::OPT_FIXUP : 0);
+    if (h->opt & sweepk::OPT_SIGMA) {
+        h->off[5] = h->out_size;                 // sigma phi
+        h->off[6] = h->off[5] + h->nodes;        // sigma J
+        h->out_size = h->off[6] + h->nodes * D.dim;
+    } else {
+        h->off[5] = h->off[6] = h->out_size;
+    }
     h->n_dir_in = D.n_dir;
 
     // alpha per outward normal (eq:alpha): sum w |Omega.n| / sum w
@@ -438,7 +447,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     for (int q = 0; q < nquad; ++q) maxq = std::max(maxq, (int)byq[q].size());
     std::vector<StreamDesc> streams;
     if (D.dim == 2) {
-        const int nw = std::min(8, std::max(1, (maxq + dirs_per_warp - 1) / dirs_per_warp));
+        int max_warps = 8;
+        if (const char* ev = getenv("SWEEP_MAXWARPS")) max_warps = std::max(1, std::min(8, atoi(ev)));  // experiment override
+        const int nw = std::min(max_warps, std::max(1, (maxq + dirs_per_warp - 1) / dirs_per_warp));
         h->block = 32 * nw;
         h->dset = nw * dirs_per_warp;
     } else {
@@ -490,13 +501,13 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     // schedule + workspace
     cudaError_t ce;
     if (D.dim == 2) {
-        const int T = sweepk::sweep2d_rows_per_strip(h->p, h->kpl), C = sweepk::sweep2d_cols_per_chunk(h->p, h->kpl);
+        const int T = sweepk::sweep2d_rows_per_strip(h->p, h->kpl), C = sweepk::sweep2d_cols_per_chunk(h->p, h->kpl, h->opt);
         h->n_strips = (h->ny + T - 1) / T;
         h->n_chunks = (h->nx + C - 1) / C;
         h->n_tasks = h->n_strips * h->n_streams;
-        h->smem = (size_t)sweepk::sweep2d_smem_bytes(h->p, h->kpl, gbk, h->dset);
+        h->smem = (size_t)sweepk::sweep2d_smem_bytes(h->p, h->kpl, gbk, h->dset, h->opt);
         int bps = 0;
-        int oe = sweepk::sweep2d_occupancy(h->p, h->log2gb, h->kpl, h->block, h->smem, &bps);
+        int oe = sweepk::sweep2d_occupancy(h->p, h->log2gb, h->kpl, h->opt, h->block, h->smem, &bps);
         if (oe || bps < 1) {
             if (oe) cuda_fail(h, (cudaError_t)oe, "occupancy");
             else h->err = "sweep2d kernel cannot be resident (registers/shared memory)";
@@ -510,7 +521,8 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * (size_t)h->n_streams * 2 * (h->n_chunks * C) * h->kpl * NT * h->block)))
             return cuda_fail(h, ce, "cudaMalloc ytr"), bail(SWEEP_E_CUDA);
     } else {
-        h->nseg = std::min(32, std::max(1, (h->nx + 15) / 16));
+        // segmented affine scan of the chain; the fixup is not affine: one segment
+        h->nseg = (h->opt & sweepk::OPT_FIXUP) ? 1 : std::min(32, std::max(1, (h->nx + 15) / 16));
         h->seglen = (h->nx + h->nseg - 1) / h->nseg;
         h->block = 32 * h->nseg;
         h->smem = sizeof(double) * (size_t)h->nseg * 96;
@@ -557,9 +569,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     return SWEEP_OK;
 }
 
-extern "C" int sweep_layout(const sweep_handle* h, size_t off[5], size_t* total) {
+extern "C" int sweep_layout(const sweep_handle* h, size_t off[7], size_t* total) {
     if (!h || !off || !total) return SWEEP_E_ARG;
-    for (int i = 0; i < 5; ++i) off[i] = h->off[i];
+    for (int i = 0; i < 7; ++i) off[i] = h->off[i];
     *total = h->out_size;
     return SWEEP_OK;
 }
@@ -588,7 +600,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.nx = h->nx;
         prm.ny = h->ny;
         prm.G = h->G;
-        prm.nx_pad = h->n_chunks * sweepk::sweep2d_cols_per_chunk(h->p, h->kpl);
+        prm.nx_pad = h->n_chunks * sweepk::sweep2d_cols_per_chunk(h->p, h->kpl, h->opt);
         prm.bulk_ok = (h->G % 2 == 0) ? 1 : 0;
         prm.n_streams = h->n_streams;
         prm.n_strips = h->n_strips;
@@ -611,7 +623,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.out_size = h->out_size;
         prm.nodes = h->nodes;
         prm.err = h->d_err;
-        e = sweepk::launch_sweep2d(h->p, h->log2gb, h->kpl, prm, h->grid, h->block, h->smem, stream);
+        e = sweepk::launch_sweep2d(h->p, h->log2gb, h->kpl, h->opt, prm, h->grid, h->block, h->smem, stream);
     } else {
         sweepk::Sweep1DParams prm;
         prm.nx = h->nx;
@@ -630,7 +642,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.out_size = h->out_size;
         prm.nodes = h->nodes;
         prm.err = h->d_err;
-        e = sweepk::launch_sweep1d(h->p, h->log2gb, prm, h->grid, h->block, h->smem, stream);
+        e = sweepk::launch_sweep1d(h->p, h->log2gb, h->opt, prm, h->grid, h->block, h->smem, stream);
     }
     if (e) return cuda_fail(h, (cudaError_t)e, "launch sweep");
     ++h->launches;

@@ -6,6 +6,10 @@
 
 namespace sweepk {
 
+// compile-time kernel options (template parameter OPT)
+constexpr int OPT_SIGMA = 1;   // append sum_g sigma_g phi_g, sum_g sigma_g J_g
+constexpr int OPT_FIXUP = 2;   // zero-and-scale negative flux fixup inside the sweep (NEXT-2)
+
 // Per (folded) direction, in sweep coordinates (every direction is mapped to
 // the (+,+) quadrant by mirroring the element order and the nodes).
 struct DirConst {
@@ -78,16 +82,28 @@ struct Sweep1DParams {
     int* err;
 };
 
-// launchers (sweep_kernels.cu); return cudaError_t as int
+// launchers (k_common.cu); return cudaError_t as int.  opt = OPT_* bits.
 int upload_modal(const ModalConsts& mc);
-int launch_sweep2d(int p, int log2lg, int k, const Sweep2DParams& prm, int grid, int block, size_t smem, void* stream);
-int launch_sweep1d(int p, int log2gb, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream);
+int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, int grid, int block, size_t smem,
+                   void* stream);
+int launch_sweep1d(int p, int log2gb, int opt, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream);
 int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream);
-int sweep2d_smem_bytes(int p, int k, int gbk, int dset);
-int sweep2d_occupancy(int p, int log2lg, int k, int block, size_t smem, int* blocks_per_sm);
+int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt);
+int sweep2d_occupancy(int p, int log2lg, int k, int opt, int block, size_t smem, int* blocks_per_sm);
 int sweep2d_rows_per_strip(int p, int k);
-int sweep2d_cols_per_chunk(int p, int k);
+int sweep2d_cols_per_chunk(int p, int k, int opt);
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
+
+// per translation unit (k2d_*.cu): kernel pointer for (log2lg, k, opt), or nullptr;
+// and the upload of that unit's copy of the modal constants
+const void* pick2d_p1(int log2lg, int k);
+const void* pick2d_p2(int log2lg, int k);
+const void* pick2d_opt_p1(int log2lg, int k, int opt);
+const void* pick2d_opt_p2(int log2lg, int k, int opt);
+int upload_modal_p1(const ModalConsts& mc);
+int upload_modal_p2(const ModalConsts& mc);
+int upload_modal_opt_p1(const ModalConsts& mc);
+int upload_modal_opt_p2(const ModalConsts& mc);
 
 }  // namespace sweepk

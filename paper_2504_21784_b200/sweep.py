@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get("SWEEP_LIB") or os.path.join(_HERE, "libsweep.so")  # 
 SWEEP_OK, E_ARG, E_QUAD, E_SIGMA, E_CUDA, E_NCCL, E_INTERNAL = range(7)
 FOLD_Z = 1
 DETERMINISTIC = 2
+SIGMA_MOMENTS = 4   # also return sum_g sigma_g phi_g, sum_g sigma_g J_g (NEXT-1)
+FIXUP = 8           # zero-and-scale negative flux fixup inside the sweep (NEXT-2)
 _NAMES = {1: "E_ARG", 2: "E_QUAD", 3: "E_SIGMA", 4: "E_CUDA", 5: "E_NCCL", 6: "E_INTERNAL"}
 
 # every symbol include/sweep.h declares
@@ -110,7 +112,7 @@ class Sweep:
     def __init__(self, dim: int, nx: int, ny: int, p: int, omega, w, n_group_local: int,
                  lx: float = 1.0, ly: float = 1.0, device: int = 0, fold_z: bool = True,
                  nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None,
-                 group_offset: int = 0, n_group_total: int | None = None):
+                 group_offset: int = 0, n_group_total: int | None = None, flags: int = 0):
         self._lib = load_library()
         self._om = np.ascontiguousarray(omega, dtype=np.float64).reshape(-1, 3)
         self._w = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
@@ -124,7 +126,7 @@ class Sweep:
         d.device, d.nranks, d.rank = device, nranks, rank
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         d.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None
-        d.flags = FOLD_Z if fold_z else 0
+        d.flags = (FOLD_Z if fold_z else 0) | int(flags)
         h = ctypes.c_void_p()
         rc = self._lib.sweep_setup(ctypes.byref(d), ctypes.byref(h))
         if rc:
@@ -132,7 +134,7 @@ class Sweep:
         self._h = h
         self.dim, self.nx, self.ny, self.p, self.G = dim, nx, (ny if dim == 2 else 1), p, n_group_local
         self.device = device
-        off = (ctypes.c_size_t * 5)()
+        off = (ctypes.c_size_t * 7)()
         tot = ctypes.c_size_t()
         self._check(self._lib.sweep_layout(self._h, off, ctypes.byref(tot)))
         self.offsets = list(off)
@@ -217,8 +219,12 @@ class Sweep:
         nel = self.nx * self.ny
         o = self.offsets
         nT = 1 if self.dim == 1 else 3
-        return {"phi": out[o[0]:o[1]].reshape(nel, n), "J": out[o[1]:o[2]].reshape(self.dim, nel, n),
-                "T": out[o[2]:o[3]].reshape(nT, nel, n), "beta": out[o[3]:o[4]], "Jplus": out[o[4]:]}
+        f = {"phi": out[o[0]:o[1]].reshape(nel, n), "J": out[o[1]:o[2]].reshape(self.dim, nel, n),
+             "T": out[o[2]:o[3]].reshape(nT, nel, n), "beta": out[o[3]:o[4]], "Jplus": out[o[4]:o[5]]}
+        if o[5] < self.out_size:
+            f["sphi"] = out[o[5]:o[6]].reshape(nel, n)
+            f["sJ"] = out[o[6]:].reshape(self.dim, nel, n)
+        return f
 
 
 def from_problem(prob, device: int = 0, fold_z: bool = True, **kw) -> Sweep:
@@ -227,11 +233,11 @@ def from_problem(prob, device: int = 0, fold_z: bool = True, **kw) -> Sweep:
                  lx=prob.lx, ly=prob.ly, device=device, fold_z=fold_z, **kw)
 
 
-def run_problem(prob, device: int = 0, fold_z: bool = True) -> np.ndarray:
+def run_problem(prob, device: int = 0, fold_z: bool = True, flags: int = 0) -> np.ndarray:
     """Convenience: copy a problem to the GPU, sweep once, return the packed output (numpy)."""
     import torch
     dev = torch.device(f"cuda:{device}")
-    with from_problem(prob, device, fold_z) as sw:
+    with from_problem(prob, device, fold_z, flags=flags) as sw:
         s = torch.from_numpy(np.ascontiguousarray(prob.sigma)).to(dev)
         q = torch.from_numpy(np.ascontiguousarray(prob.q)).to(dev)
         f = torch.from_numpy(np.ascontiguousarray(prob.inflow)).to(dev)

@@ -9,7 +9,7 @@ TINY = 1e-8          # a field whose reference norm is below TINY * |phi| is com
 ABS_TOL = 1e-13      # ... with |delta| <= ABS_TOL * |phi|
 
 
-def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
+def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int, sigma_moments: bool = False) -> dict:
     n = (p + 1) ** dim
     nel = nx * (ny if dim == 2 else 1)
     nodes = nel * n
@@ -21,30 +21,39 @@ def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
         o += nodes
     f["beta"] = out[o:o + nb]
     f["Jplus"] = out[o + nb:o + 2 * nb]
-    assert o + 2 * nb == out.size, (o + 2 * nb, out.size)
+    o += 2 * nb
+    if sigma_moments:
+        for nm in ["sphi"] + [f"sJ{c}" for c in "xy"[:dim]]:
+            f[nm] = out[o:o + nodes]
+            o += nodes
+    assert o == out.size, (o, out.size)
     return f
 
 
-def field_errors(got: np.ndarray, ref: np.ndarray, dim: int, nx: int, ny: int, p: int) -> dict:
-    """{field: (error, kind)} with kind 'rel' (|d|/|ref|) or 'abs_phi' (|d|/|phi|)."""
-    fg, fr = fields(got, dim, nx, ny, p), fields(ref, dim, nx, ny, p)
+def field_errors(got: np.ndarray, ref: np.ndarray, dim: int, nx: int, ny: int, p: int,
+                 sigma_moments: bool = False) -> dict:
+    """{field: (error, kind)} with kind 'rel' (|d|/|ref|) or 'abs_phi' (|d|/|phi|).
+    (sigma-weighted fields are compared relative to their own norm, or to |sphi| when tiny)"""
+    fg, fr = fields(got, dim, nx, ny, p, sigma_moments), fields(ref, dim, nx, ny, p, sigma_moments)
     phi = max(np.abs(fr["phi"]).max(), 1e-300)
+    sphi = max(np.abs(fr["sphi"]).max(), 1e-300) if sigma_moments else phi
     res = {}
     for k in fr:
+        base = sphi if k.startswith("s") else phi
         d = np.abs(fg[k] - fr[k]).max() if fr[k].size else 0.0
         if not np.isfinite(d):
             res[k] = (np.inf, "rel")
             continue
         nref = np.abs(fr[k]).max() if fr[k].size else 0.0
-        if nref >= TINY * phi:
+        if nref >= TINY * base:
             res[k] = (d / nref, "rel")
         else:
-            res[k] = (d / phi, "abs_phi")
+            res[k] = (d / base, "abs_phi")
     return res
 
 
-def assert_parity(got, ref, dim, nx, ny, p, tol=TOL):
-    errs = field_errors(got, ref, dim, nx, ny, p)
+def assert_parity(got, ref, dim, nx, ny, p, tol=TOL, sigma_moments=False):
+    errs = field_errors(got, ref, dim, nx, ny, p, sigma_moments)
     bad = {k: v for k, v in errs.items() if v[0] > (tol if v[1] == "rel" else ABS_TOL)}
     assert not bad, f"parity failed: {bad} (all: {errs})"
     return errs
