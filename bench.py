@@ -54,6 +54,40 @@ def flops_per_edg(p: int, dim: int, n_dir_quad: int, gb: int) -> float:
     return 20.0 + 2 * 3 * (p + 1)
 
 
+def option_flops_per_edg(p: int, dim: int, opts: set) -> float:
+    """Extra flops per (element, distinct direction, group) of the NEXT-row options:
+    sigma moments: sigma * u accumulated per modal/nodal value (n FMA); fixup, p = 2:
+    the nodal check (V (x) V) u (81 FMA; the rare back transform is not credited)."""
+    n = (p + 1) ** dim
+    extra = 0.0
+    if "sigma" in opts:
+        extra += 2 * n
+    if "fixup" in opts and p == 2 and dim == 2:
+        extra += 2 * 81
+    return extra
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def profiled_traffic(cfg: int, opts: set):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the sweep kernel from the
+    committed ncu --set full capture (profiles/traffic_C<cfg>.json), or None."""
+    if opts:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_C{cfg}.json")) as f:
+            t = json.load(f)
+        return {"bytes_per_launch": t["dram_bytes_per_launch"], "source": t["source"]}
+    except Exception:
+        return None
+
+
 def algorithmic_bytes(prob) -> int:
     """Inputs read once + gray output written once."""
     n_in = prob.sigma.size + prob.q.size + prob.inflow.size
@@ -150,7 +184,7 @@ def run_reference(args, prob) -> dict:
     dt = (time.perf_counter() - t0) / args.steps
     v = sample.unknowns / dt
     desc = f"{prob.name} mesh and all {prob.n_dir} directions, 1 of {prob.G} groups ({sample.unknowns} unknowns)"
-    return {"metric": METRIC, "value": v, "unit": "unknowns/s", "n_gpus": 0, "steps": args.steps,
+    return {"metric": METRIC, "value": v, "unit": "unknowns/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "impl": "reference",
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config], "sample": desc},
@@ -169,7 +203,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--opts", default="", help="comma list of NEXT-row options: sigma (sigma-weighted moments), "
+                                                 "fixup (zero-and-scale negative flux fixup)")
     args = ap.parse_args()
+    opts = {o for o in args.opts.split(",") if o}
+    if opts - {"sigma", "fixup"}:
+        ap.error(f"unknown --opts {opts - {'sigma', 'fixup'}}")
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
 
@@ -199,9 +238,10 @@ def main():
         obj = [pk.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
+    flags = (pk.SIGMA_MOMENTS if "sigma" in opts else 0) | (pk.FIXUP if "fixup" in opts else 0)
     sw = pk.Sweep(prob.dim, prob.nx, prob.ny, prob.p, prob.omega, prob.w, g1 - g0, lx=prob.lx, ly=prob.ly,
                   device=local, fold_z=True, nranks=ws, rank=rank, nccl_id=nid, group_offset=g0,
-                  n_group_total=prob.G)
+                  n_group_total=prob.G, flags=flags)
     stream = torch.cuda.current_stream()
     sig = torch.from_numpy(shard.sigma).to(dev)
     q = torch.from_numpy(shard.q).to(dev)
@@ -277,10 +317,13 @@ def main():
     if rank == 0:
         nd = distinct_dirs(prob)
         gb = min(32, 1 << max(0, (shard.G - 1).bit_length()))
-        f_edg = flops_per_edg(prob.p, prob.dim, nd // (4 if prob.dim == 2 else 2), gb)
+        f_edg = flops_per_edg(prob.p, prob.dim, nd // (4 if prob.dim == 2 else 2), gb) + \
+            option_flops_per_edg(prob.p, prob.dim, opts)
         flops = f_edg * prob.n_el * nd * prob.G / ws          # per rank per launch (folded)
         achieved_tf = flops / (sweep_ms * 1e-3) / 1e12
         peak_nominal = SMS * FP64_FMA_PER_SM_CLK * 2 * SM_MAX_MHZ * 1e6 / 1e12
+        peaks = measured_peaks()
+        traffic = profiled_traffic(args.config, opts)
         try:
             peak_probe = pk.fp64_probe(local)
         except Exception:
@@ -298,13 +341,16 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD[args.config], "fold_z": True, "distinct_directions": nd,
+            "config": {"workload": WORKLOAD[args.config] + (f" + options {sorted(opts)}" if opts else ""),
+                       "fold_z": True, "distinct_directions": nd,
                        "unknowns": prob.unknowns, "groups_per_rank": g1 - g0,
                        "parallelism": f"group-sharded x{ws}" + (" + NCCL all-reduce" if ws > 1 else ""),
                        "l2": ("inputs %.2f GB > 126 MB L2, no flush" % (in_bytes / 1e9)) if not flush.numel()
                        else "256 MB L2 flush before every step (outside the kernel timings)"},
             "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_nominal, "unit": "TFLOP/s",
-                         "frac": achieved_tf / peak_nominal, "traffic": None,
+                         "frac": achieved_tf / peak_nominal,
+                         "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
                          "kernel": "sweep2d_kernel" if prob.dim == 2 else "sweep1d_kernel",
                          "kernel_ms": sweep_ms, "flops_per_launch": flops, "flops_per_edg": f_edg,
                          "peak_source": "FP64 pipe: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (DESIGN.md §5)",
@@ -312,7 +358,8 @@ def main():
                          "frac_of_probe": (achieved_tf / peak_probe) if peak_probe else None,
                          "hbm": {"algorithmic_bytes": algorithmic_bytes(prob),
                                  "achieved_gbs": algorithmic_bytes(prob) / ws / (sweep_ms * 1e-3) / 1e9,
-                                 "peak_gbs_measured": 6557.1}},
+                                 "peak_gbs_measured": peaks.get("hbm_gbs"),
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (b.copy_(a), read+write)"}},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk,
             "step_breakdown_ms": {"sweep": float(kt[:, 0].mean()), "finalize": float(kt[:, 1].mean()),
