@@ -6,7 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <type_traits>
-#include "../paper_2504_21784_b200/csrc/sweep_kernels.cu"
+#include "../paper_2504_21784_b200/csrc/sweep_device.cuh"
 
 using namespace sweepk;
 
@@ -106,7 +106,7 @@ int main() {
         mc.V1re[a] = 0.25;
         mc.V1im[a] = 0.125 * a;
     }
-    upload_modal(mc);
+    cudaMemcpyToSymbol(cM, &mc, sizeof(ModalConsts));  // this unit's copy of the constants
     run<2, 4, true, 1>("K2 T4 red LG32", 8, 1, d);
     run<4, 2, true, 1, 16>("K4 T2 red LG16", 8, 1, d);
     run<4, 4, true, 1, 16>("K4 T4 red LG16", 8, 1, d);

@@ -1,7 +1,6 @@
 """Experiment builds of libsweep.so with -D overrides, into build/<name>.so (used with SWEEP_LIB=...).
 usage: python scripts/build_variants.py name1:-DFOO=1,-DBAR name2: ..."""
 import os, subprocess, sys
-from concurrent.futures import ThreadPoolExecutor
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2504_21784_b200 import build as b
@@ -10,9 +9,11 @@ def one(spec):
     name, _, defs = spec.partition(":")
     flags = [d for d in defs.split(",") if d]
     out = os.path.join(ROOT, "build", name + ".so")
-    cmd = [b.nvcc(), *b.NVCC_FLAGS, *flags, "-I", os.path.join(ROOT, "include"), "-o", out, *b.SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    return name, r.returncode, r.stderr[-2000:]
-with ThreadPoolExecutor(len(sys.argv) - 1) as ex:
-    for name, rc, err in ex.map(one, sys.argv[1:]):
-        print(name, "ok" if rc == 0 else "FAIL\n" + err)
+    try:
+        b.build(extra=flags, out=out)
+        return name, 0, ""
+    except subprocess.CalledProcessError as e:
+        return name, 1, str(e)
+for spec in sys.argv[1:]:   # each build already compiles its units in parallel
+    name, rc, err = one(spec)
+    print(name, "ok" if rc == 0 else "FAIL\n" + err)
