@@ -204,11 +204,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--opts", default="", help="comma list of NEXT-row options: sigma (sigma-weighted moments), "
-                                                 "fixup (zero-and-scale negative flux fixup)")
+                                                 "fixup (zero-and-scale negative flux fixup), halfrange "
+                                                 "(half-range moments of the consistent method)")
     args = ap.parse_args()
     opts = {o for o in args.opts.split(",") if o}
-    if opts - {"sigma", "fixup"}:
-        ap.error(f"unknown --opts {opts - {'sigma', 'fixup'}}")
+    if opts - {"sigma", "fixup", "halfrange"}:
+        ap.error(f"unknown --opts {opts - {'sigma', 'fixup', 'halfrange'}}")
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
 
@@ -238,7 +239,8 @@ def main():
         obj = [pk.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    flags = (pk.SIGMA_MOMENTS if "sigma" in opts else 0) | (pk.FIXUP if "fixup" in opts else 0)
+    flags = ((pk.SIGMA_MOMENTS if "sigma" in opts else 0) | (pk.FIXUP if "fixup" in opts else 0) |
+             (pk.HALF_RANGE if "halfrange" in opts else 0))
     sw = pk.Sweep(prob.dim, prob.nx, prob.ny, prob.p, prob.omega, prob.w, g1 - g0, lx=prob.lx, ly=prob.ly,
                   device=local, fold_z=True, nranks=ws, rank=rank, nccl_id=nid, group_offset=g0,
                   n_group_total=prob.G, flags=flags)

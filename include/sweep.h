@@ -33,12 +33,21 @@
  * Output packing (doubles), all gray = summed over every group of every rank:
  *   phi[N_el][n] | J[dim][N_el][n] | T[nT][N_el][n] | beta[N_bnode] | Jplus[N_bnode]
  *   [ | sphi[N_el][n] | sJ[dim][N_el][n]    with SWEEP_SIGMA_MOMENTS ]
+ *   [ | HR[10 or 2][N_el][n]                 with SWEEP_HALF_RANGE ]
  *   nT = 1 (dim 1: T_xx) or 3 (dim 2: T_xx, T_xy, T_yy; T_zz = -T_xx - T_yy).
  *   sphi = sum_g sigma_t,g phi_g and sJ = sum_g sigma_t,g J_g are the sigma-weighted
  *   gray moments the gray low-order system takes from the sweep: the numerator of
  *   sigma_E (eq:sigmaE) and the high-order part of the additive
  *   multigroup correction sum_g (sigma_F - sigma_g) F_g (eq:additive_mg_correction,
  *   PAPER.md:197-203, :247).  sigma_t excludes 1/(c dt).
+ *   HR are the half-range moments of the consistent low-order method
+ *   (PAPER.md:424-428), at every node (= each element's own trace at its face nodes):
+ *     dim 2: F+_{+x}[x,y], P+_{+x}[xx,xy,yy], F+_{+y}[x,y], P+_{+y}[xx,xy,yy]
+ *     dim 1: F+ , P+            (F+_n = sum_g sum_{Omega.n>0} w Omega psi,
+ *                                P+_n = sum_g sum_{Omega.n>0} w Omega Omega psi;
+ *   Omega.n = 0 counts as + (reading R23); the minus halves are J - F+ and
+ *   (T + phi I/3) - P+, and sum w |Omega.n| psi = 2 F+_n . n - J.n gives beta on
+ *   every interior face, so the jumps the consistent method needs follow).
  *
  * Every function returns an int status (SWEEP_OK = 0) and never aborts or
  * throws across the ABI; sweep_last_error gives the message of the last
@@ -72,6 +81,7 @@ enum {
 #define SWEEP_DETERMINISTIC 2u   /* accepted for API compatibility: every reduction already runs in a
                                     fixed order, so results are bitwise repeatable in all modes */
 #define SWEEP_SIGMA_MOMENTS 4u   /* also return sphi, sJ (see the output packing above) */
+#define SWEEP_HALF_RANGE 16u     /* also return the half-range moments HR (see the output packing) */
 #define SWEEP_FIXUP 8u           /* zero-and-scale negative flux fixup inside the sweep (PAPER.md:987,
                                     :1321): after every element solve, negative nodal values are set
                                     to 0 and the others scaled to keep the element integral
@@ -95,7 +105,7 @@ typedef struct {
     int device;              /* CUDA device ordinal */
     int nranks, rank;        /* nranks = 1: no collective; > 1: NCCL all-reduce of the gray output */
     const void *nccl_id;     /* 128-byte ncclUniqueId created by rank 0 and broadcast (nranks > 1), else NULL */
-    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC | SWEEP_SIGMA_MOMENTS | SWEEP_FIXUP */
+    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC | SWEEP_SIGMA_MOMENTS | SWEEP_FIXUP | SWEEP_HALF_RANGE */
 } sweep_desc;
 
 /* Validate the description, fold/sort directions into sweep quadrants,
@@ -105,9 +115,10 @@ typedef struct {
  * *out receives the handle, or NULL on failure. */
 int sweep_setup(const sweep_desc *desc, sweep_handle **out);
 
-/* Offsets (in doubles) of phi, J, T, beta, Jplus, sphi, sJ inside the packed
- * output, and its total length (off[5] = off[6] = total without SWEEP_SIGMA_MOMENTS). */
-int sweep_layout(const sweep_handle *h, size_t off[7], size_t *total_doubles);
+/* Offsets (in doubles) of phi, J, T, beta, Jplus, sphi, sJ, HR inside the packed
+ * output, and its total length (an option's offsets equal the next field's offset
+ * when the option is off). */
+int sweep_layout(const sweep_handle *h, size_t off[8], size_t *total_doubles);
 
 /* One sweep + fused closures, enqueued asynchronously on cuda_stream
  * (a cudaStream_t; NULL = legacy default stream).  Device pointers, borrowed,

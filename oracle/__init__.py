@@ -72,6 +72,7 @@ def _c(a) -> np.ndarray:
 
 SIGMA_MOMENTS = 1   # opts bit 0: append sum_g sigma_g phi_g, sum_g sigma_g J_g (NEXT-1)
 FIXUP = 2           # opts bit 1: zero-and-scale negative flux fixup inside the sweep (NEXT-2)
+HALF_RANGE = 4      # opts bit 2: half-range moments F+, P+ of the consistent method (NEXT-3)
 
 
 def out_size(dim: int, nx: int, ny: int, p: int, opts: int = 0) -> int:
@@ -139,5 +140,8 @@ def unpack(out: np.ndarray, dim: int, nx: int, ny: int, p: int, opts: int = 0) -
     if opts & SIGMA_MOMENTS:
         f["sphi"] = out[o:o + nodes].reshape(nel, n); o += nodes
         f["sJ"] = out[o:o + dim * nodes].reshape(dim, nel, n); o += dim * nodes
+    if opts & HALF_RANGE:
+        nr = 10 if dim == 2 else 2
+        f["HR"] = out[o:o + nr * nodes].reshape(nr, nel, n); o += nr * nodes
     assert o == out.size
     return f

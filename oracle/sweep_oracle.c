@@ -32,6 +32,10 @@
  *   negative, negatives are set to 0 and the rest scaled so the element integral
  *   sum_k W_k psi_k is preserved; a non-positive integral zeroes the element.  The
  *   fixed-up values are what the downwind elements see.
+ *   (opts bit 2): the half-range moments of the consistent
+ *   low-order method at every node,
+ *       F+_n = sum_g sum_{Omega.n > 0} w Omega psi,  P+_n = sum_g sum_{Omega.n > 0} w Omega Omega psi
+ *   for n = +x, +y (dim 1: n = +x), with Omega.n = 0 counted as + (reading R23).
  *
  * How (deliberately plain): for each (d,g), elements are visited in upwind
  * nested-loop order; the element matrix is assembled UNSCALED straight from
@@ -293,7 +297,8 @@ static int setup(prob *P, int dim, int nx, int ny, double lx, double ly, int p, 
 static size_t out_size(const prob *P, size_t *nodes, int *nT, int opts) {
     *nodes = (size_t)P->nx * P->ny * P->n;
     *nT = (P->dim == 1) ? 1 : 3;
-    return (*nodes) * (1 + P->dim + *nT) + 2 * (size_t)P->nbnode + ((opts & 1) ? (*nodes) * (1 + P->dim) : 0);
+    return (*nodes) * (1 + P->dim + *nT) + 2 * (size_t)P->nbnode + ((opts & 1) ? (*nodes) * (1 + P->dim) : 0) +
+           ((opts & 4) ? (*nodes) * (P->dim == 2 ? 10 : 2) : 0);
 }
 
 int oracle_out_size2(int dim, int nx, int ny, int p, int opts) {
@@ -301,7 +306,8 @@ int oracle_out_size2(int dim, int nx, int ny, int p, int opts) {
     int nel = (dim == 2) ? nx * ny : nx;
     int nT = (dim == 1) ? 1 : 3;
     int nb = (dim == 1) ? 2 : 2 * (nx + ny) * (p + 1);
-    return nel * n * (1 + dim + nT) + 2 * nb + ((opts & 1) ? nel * n * (1 + dim) : 0);
+    return nel * n * (1 + dim + nT) + 2 * nb + ((opts & 1) ? nel * n * (1 + dim) : 0) +
+           ((opts & 4) ? nel * n * (dim == 2 ? 10 : 2) : 0);
 }
 
 int oracle_out_size(int dim, int nx, int ny, int p) { return oracle_out_size2(dim, nx, ny, p, 0); }
@@ -350,6 +356,8 @@ int oracle_sweep2(int dim, int nx, int ny, double lx, double ly, int p, int ndir
     const int ncomp = 1 + dim + nT;
     const int sig_mom = opts & 1, fixup = (opts >> 1) & 1;
     const size_t off_sig = (size_t)ncomp * nodes + 2 * (size_t)P.nbnode;  /* sphi, then sJ */
+    const int half = (opts >> 2) & 1;
+    const size_t off_hr = off_sig + (sig_mom ? (size_t)(1 + dim) * nodes : 0);
 
     /* per-direction closure coefficients, precomputed as w (Omega Omega - I/3) (R16) */
     double *coef = (double *)malloc(sizeof(double) * (size_t)ndir * 6);
@@ -430,6 +438,33 @@ int oracle_sweep2(int dim, int nx, int ny, double lx, double ly, int p, int ndir
             for (size_t v = 0; v < nodes; ++v) {
                 const double ps = psi[v];
                 for (int m = 0; m < ncomp; ++m) nadd(&S[m * nodes + v], &C[m * nodes + v], c[m] * ps);
+            }
+            if (half) {
+                /* half-range moments: directions with Omega_x >= 0 (rows 0-4), Omega_y >= 0 (rows 5-9);
+                 * dim 1: mu >= 0 (rows 0-1) */
+                const double ox = omega[3 * d], oy = (dim == 2) ? omega[3 * d + 1] : 0.0, wd = w[d];
+                double row[10];
+                int nrow;
+                if (dim == 2) {
+                    const double vx[5] = {wd * ox, wd * oy, wd * ox * ox, wd * ox * oy, wd * oy * oy};
+                    for (int m = 0; m < 5; ++m) {
+                        row[m] = (ox >= 0.0) ? vx[m] : 0.0;
+                        row[5 + m] = (oy >= 0.0) ? vx[m] : 0.0;
+                    }
+                    nrow = 10;
+                } else {
+                    row[0] = (ox >= 0.0) ? wd * ox : 0.0;
+                    row[1] = (ox >= 0.0) ? wd * ox * ox : 0.0;
+                    nrow = 2;
+                }
+                for (size_t v = 0; v < nodes; ++v) {
+                    const double ps = psi[v];
+                    for (int m = 0; m < nrow; ++m) {
+                        if (row[m] == 0.0) continue;
+                        const size_t o = off_hr + m * nodes + v;
+                        nadd(&S[o], &C[o], row[m] * ps);
+                    }
+                }
             }
             if (sig_mom) {
                 /* sum_g sigma_g (w, w Omega) psi: sigma_g of the node's element, no 1/(c dt) */

@@ -5,16 +5,71 @@
 namespace sweepk {
 
 // ------------------------------------------------------------------ finalize
-__global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, size_t n, double* __restrict__ out,
-                                int* err) {
+__global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, size_t stride, size_t n,
+                                double* __restrict__ out, int* err) {
     bool bad = false;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         double acc = 0.0;
-        for (int s = 0; s < n_slabs; ++s) acc += __ldcs(slabs + (size_t)s * n + i);
+        for (int s = 0; s < n_slabs; ++s) acc += __ldcs(slabs + (size_t)s * stride + i);
         out[i] = acc;
         bad |= !(fabs(acc) < 1.0e300);
     }
     if (bad) atomicOr(err, 2);
+}
+
+// ------------------------------------------------------------------ half-range moments (NEXT-3)
+// Every slab holds one stream's contribution, and a stream is one sweep quadrant
+// (half-range in 1-D): all its directions have the same signs of Omega_x, Omega_y.
+// The half-range face moments of the consistent low-order method
+//     F+_n = sum_g sum_{Omega.n > 0} w Omega psi,   P+_n = sum_g sum_{Omega.n > 0} w Omega Omega psi
+// for n = +x, +y are therefore sums of whole slabs: J and P = T + phi I / 3 of the
+// streams with Omega_x >= 0 (resp. Omega_y >= 0), evaluated at every node (each
+// element's own trace at its face nodes).  F-, P- = full minus plus.
+// out rows (2-D): Fx+[x,y], Px+[xx,xy,yy], Fy+[x,y], Py+[xx,xy,yy]; (1-D): F+, P+.
+__global__ void halfrange_kernel(const double* __restrict__ slabs, int n_slabs, size_t stride,
+                                 const StreamDesc* __restrict__ streams, size_t nodes, int dim,
+                                 double* __restrict__ out) {
+    const double third = 1.0 / 3.0;
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += (size_t)gridDim.x * blockDim.x) {
+        if (dim == 2) {
+            double a[10];
+#pragma unroll
+            for (int m = 0; m < 10; ++m) a[m] = 0.0;
+            for (int s = 0; s < n_slabs; ++s) {
+                const double* sl = slabs + (size_t)s * stride;
+                const int q = streams[s].quadrant;
+                const double ph = sl[v], jx = sl[nodes + v], jy = sl[2 * nodes + v];
+                const double pxx = sl[3 * nodes + v] + third * ph, pxy = sl[4 * nodes + v],
+                             pyy = sl[5 * nodes + v] + third * ph;
+                if (!(q & 1)) {
+                    a[0] += jx;
+                    a[1] += jy;
+                    a[2] += pxx;
+                    a[3] += pxy;
+                    a[4] += pyy;
+                }
+                if (!(q & 2)) {
+                    a[5] += jx;
+                    a[6] += jy;
+                    a[7] += pxx;
+                    a[8] += pxy;
+                    a[9] += pyy;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 10; ++m) out[(size_t)m * nodes + v] = a[m];
+        } else {
+            double f = 0.0, pp = 0.0;
+            for (int s = 0; s < n_slabs; ++s) {
+                if (streams[s].quadrant & 1) continue;
+                const double* sl = slabs + (size_t)s * stride;
+                f += sl[nodes + v];
+                pp += sl[2 * nodes + v] + third * sl[v];
+            }
+            out[v] = f;
+            out[nodes + v] = pp;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ launchers
@@ -92,12 +147,22 @@ int launch_sweep1d(int p, int log2gb, int opt, const Sweep1DParams& prm, int gri
     return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
 }
 
-int launch_finalize(const double* slabs, int n_slabs, size_t out_size, double* out, int* err, void* stream) {
+int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, void* stream) {
     const int block = 256;
-    size_t want = (out_size + block - 1) / block;
+    size_t want = (n + block - 1) / block;
     int grid = (int)(want < 148 * 8 ? want : 148 * 8);
     if (grid < 1) grid = 1;
-    finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, out_size, out, err);
+    finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, n, out, err);
+    return (int)cudaGetLastError();
+}
+
+int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes, int dim,
+                     double* out, void* stream) {
+    const int block = 256;
+    size_t want = (nodes + block - 1) / block;
+    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+    if (grid < 1) grid = 1;
+    halfrange_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, nodes, dim, out);
     return (int)cudaGetLastError();
 }
 

@@ -90,7 +90,8 @@ struct sweep_handle {
     int dim, nx, ny, p, n, np1, nbnode, G, device, nranks, rank;
     double lx, ly, hx, hy;
     unsigned flags;
-    size_t nodes, out_size, off[7];
+    size_t nodes, out_size, off[8];
+    size_t sum_size = 0;  // leading part of the output summed over slabs (all but the half-range rows)
     int opt = 0;  // sweepk::OPT_* bits from the flags
     int n_dir_in, n_dir_eff;
     // schedule
@@ -345,6 +346,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     } else {
         h->off[5] = h->off[6] = h->out_size;
     }
+    h->sum_size = h->out_size;
+    h->off[7] = h->out_size;  // half-range rows (SWEEP_HALF_RANGE): 10 (dim 2) or 2 (dim 1) per node
+    if (D.flags & SWEEP_HALF_RANGE) h->out_size += h->nodes * (D.dim == 2 ? 10 : 2);
     h->n_dir_in = D.n_dir;
 
     // alpha per outward normal (eq:alpha): sum w |Omega.n| / sum w
@@ -569,9 +573,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     return SWEEP_OK;
 }
 
-extern "C" int sweep_layout(const sweep_handle* h, size_t off[7], size_t* total) {
+extern "C" int sweep_layout(const sweep_handle* h, size_t off[8], size_t* total) {
     if (!h || !off || !total) return SWEEP_E_ARG;
-    for (int i = 0; i < 7; ++i) off[i] = h->off[i];
+    for (int i = 0; i < 8; ++i) off[i] = h->off[i];
     *total = h->out_size;
     return SWEEP_OK;
 }
@@ -647,9 +651,15 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
     if (e) return cuda_fail(h, (cudaError_t)e, "launch sweep");
     ++h->launches;
     if (evs) cudaEventRecord(evs[1], st);
-    e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->d_out, h->d_err, stream);
+    e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->sum_size, h->d_out, h->d_err, stream);
     if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");
     ++h->launches;
+    if (h->out_size > h->sum_size) {
+        e = sweepk::launch_halfrange(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->nodes, h->dim,
+                                     h->d_out + h->sum_size, stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "launch halfrange");
+        ++h->launches;
+    }
     if (evs) cudaEventRecord(evs[2], st);
     if (h->nranks > 1) {
         int r = g_nccl.allReduce(h->d_out, h->d_out, h->out_size, kNcclFloat64, kNcclSum, h->comm, st);

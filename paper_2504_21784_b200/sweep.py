@@ -19,6 +19,7 @@ FOLD_Z = 1
 DETERMINISTIC = 2
 SIGMA_MOMENTS = 4   # also return sum_g sigma_g phi_g, sum_g sigma_g J_g (NEXT-1)
 FIXUP = 8           # zero-and-scale negative flux fixup inside the sweep (NEXT-2)
+HALF_RANGE = 16     # also return the half-range moments F+, P+ of the consistent method (NEXT-3)
 _NAMES = {1: "E_ARG", 2: "E_QUAD", 3: "E_SIGMA", 4: "E_CUDA", 5: "E_NCCL", 6: "E_INTERNAL"}
 
 # every symbol include/sweep.h declares
@@ -134,7 +135,7 @@ class Sweep:
         self._h = h
         self.dim, self.nx, self.ny, self.p, self.G = dim, nx, (ny if dim == 2 else 1), p, n_group_local
         self.device = device
-        off = (ctypes.c_size_t * 7)()
+        off = (ctypes.c_size_t * 8)()
         tot = ctypes.c_size_t()
         self._check(self._lib.sweep_layout(self._h, off, ctypes.byref(tot)))
         self.offsets = list(off)
@@ -221,9 +222,11 @@ class Sweep:
         nT = 1 if self.dim == 1 else 3
         f = {"phi": out[o[0]:o[1]].reshape(nel, n), "J": out[o[1]:o[2]].reshape(self.dim, nel, n),
              "T": out[o[2]:o[3]].reshape(nT, nel, n), "beta": out[o[3]:o[4]], "Jplus": out[o[4]:o[5]]}
-        if o[5] < self.out_size:
+        if o[5] < o[7]:
             f["sphi"] = out[o[5]:o[6]].reshape(nel, n)
-            f["sJ"] = out[o[6]:].reshape(self.dim, nel, n)
+            f["sJ"] = out[o[6]:o[7]].reshape(self.dim, nel, n)
+        if o[7] < self.out_size:
+            f["HR"] = out[o[7]:].reshape(-1, nel, n)
         return f
 
 

@@ -9,7 +9,8 @@ TINY = 1e-8          # a field whose reference norm is below TINY * |phi| is com
 ABS_TOL = 1e-13      # ... with |delta| <= ABS_TOL * |phi|
 
 
-def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int, sigma_moments: bool = False) -> dict:
+def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int, sigma_moments: bool = False,
+           half_range: bool = False) -> dict:
     n = (p + 1) ** dim
     nel = nx * (ny if dim == 2 else 1)
     nodes = nel * n
@@ -26,20 +27,27 @@ def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int, sigma_moments: b
         for nm in ["sphi"] + [f"sJ{c}" for c in "xy"[:dim]]:
             f[nm] = out[o:o + nodes]
             o += nodes
+    if half_range:
+        names = (["F+x_x", "F+x_y", "P+x_xx", "P+x_xy", "P+x_yy", "F+y_x", "F+y_y", "P+y_xx", "P+y_xy", "P+y_yy"]
+                 if dim == 2 else ["F+", "P+"])
+        for nm in names:
+            f[nm] = out[o:o + nodes]
+            o += nodes
     assert o == out.size, (o, out.size)
     return f
 
 
 def field_errors(got: np.ndarray, ref: np.ndarray, dim: int, nx: int, ny: int, p: int,
-                 sigma_moments: bool = False) -> dict:
+                 sigma_moments: bool = False, half_range: bool = False) -> dict:
     """{field: (error, kind)} with kind 'rel' (|d|/|ref|) or 'abs_phi' (|d|/|phi|).
     (sigma-weighted fields are compared relative to their own norm, or to |sphi| when tiny)"""
-    fg, fr = fields(got, dim, nx, ny, p, sigma_moments), fields(ref, dim, nx, ny, p, sigma_moments)
+    fg = fields(got, dim, nx, ny, p, sigma_moments, half_range)
+    fr = fields(ref, dim, nx, ny, p, sigma_moments, half_range)
     phi = max(np.abs(fr["phi"]).max(), 1e-300)
     sphi = max(np.abs(fr["sphi"]).max(), 1e-300) if sigma_moments else phi
     res = {}
     for k in fr:
-        base = sphi if k.startswith("s") else phi
+        base = sphi if k in ("sphi", "sJx", "sJy") else phi
         d = np.abs(fg[k] - fr[k]).max() if fr[k].size else 0.0
         if not np.isfinite(d):
             res[k] = (np.inf, "rel")
@@ -52,8 +60,8 @@ def field_errors(got: np.ndarray, ref: np.ndarray, dim: int, nx: int, ny: int, p
     return res
 
 
-def assert_parity(got, ref, dim, nx, ny, p, tol=TOL, sigma_moments=False):
-    errs = field_errors(got, ref, dim, nx, ny, p, sigma_moments)
+def assert_parity(got, ref, dim, nx, ny, p, tol=TOL, sigma_moments=False, half_range=False):
+    errs = field_errors(got, ref, dim, nx, ny, p, sigma_moments, half_range)
     bad = {k: v for k, v in errs.items() if v[0] > (tol if v[1] == "rel" else ABS_TOL)}
     assert not bad, f"parity failed: {bad} (all: {errs})"
     return errs

@@ -1,6 +1,7 @@
 """GPU parity of the NEXT rows (-m gpu) through the C-ABI against the oracle:
   NEXT-1  SWEEP_SIGMA_MOMENTS: sum_g sigma_g phi_g, sum_g sigma_g J_g appended;
-  NEXT-2  SWEEP_FIXUP: zero-and-scale negative flux fixup inside the sweep.
+  NEXT-2  SWEEP_FIXUP: zero-and-scale negative flux fixup inside the sweep;
+  NEXT-3  SWEEP_HALF_RANGE: half-range moments F+, P+ of the consistent method.
 Shapes cover both kernels (1-D scan / 2-D strip pipeline), both orders, the
 1-group-per-lane and the many-group (16 lanes x 4 groups) layouts, ragged
 tails, and problems whose unfixed solution goes negative."""
@@ -16,7 +17,7 @@ from tests.parity import assert_parity
 
 pytestmark = pytest.mark.gpu
 
-SIG, FIX = oracle.SIGMA_MOMENTS, oracle.FIXUP
+SIG, FIX, HR = oracle.SIGMA_MOMENTS, oracle.FIXUP, oracle.HALF_RANGE
 
 
 @pytest.fixture(scope="module")
@@ -32,13 +33,15 @@ def pk():
 
 
 def _flags(pk, opts):
-    return (pk.SIGMA_MOMENTS if opts & SIG else 0) | (pk.FIXUP if opts & FIX else 0)
+    return ((pk.SIGMA_MOMENTS if opts & SIG else 0) | (pk.FIXUP if opts & FIX else 0) |
+            (pk.HALF_RANGE if opts & HR else 0))
 
 
 def check(pk, prob, opts):
     ref = oracle.sweep(prob, opts=opts)
     got = pk.run_problem(prob, flags=_flags(pk, opts))
-    return assert_parity(got, ref, prob.dim, prob.nx, prob.ny, prob.p, sigma_moments=bool(opts & SIG))
+    return assert_parity(got, ref, prob.dim, prob.nx, prob.ny, prob.p, sigma_moments=bool(opts & SIG),
+                         half_range=bool(opts & HR))
 
 
 def negative_problem(dim, p, nx, ny, G, seed=0, omega=None, w=None):
@@ -54,7 +57,7 @@ def negative_problem(dim, p, nx, ny, G, seed=0, omega=None, w=None):
 SMALL = [(1, 1, 40, 1, 3), (1, 2, 33, 1, 5), (2, 1, 9, 7, 3), (2, 2, 7, 9, 2), (2, 2, 1, 1, 1), (1, 1, 300, 1, 8)]
 
 
-@pytest.mark.parametrize("opts", [SIG, FIX, SIG | FIX])
+@pytest.mark.parametrize("opts", [SIG, FIX, HR, SIG | FIX | HR])
 @pytest.mark.parametrize("dim,p,nx,ny,G", SMALL)
 def test_options_random_small(pk, opts, dim, p, nx, ny, G):
     prob = random_problem(300 + nx + G, dim, nx, ny, p, 7, G)
@@ -71,7 +74,7 @@ def test_fixup_on_negative_solutions(pk, opts, dim, p, nx, ny):
     check(pk, prob, opts)
 
 
-@pytest.mark.parametrize("opts", [SIG, FIX, SIG | FIX])
+@pytest.mark.parametrize("opts", [SIG, FIX, HR | SIG, SIG | FIX | HR])
 @pytest.mark.parametrize("nx,ny,G", [(13, 7, 64), (9, 17, 66), (20, 3, 128)])
 def test_options_many_group_layout(pk, opts, nx, ny, G):
     om, w = synth.product_set(8, 16)
@@ -85,7 +88,16 @@ def test_options_many_group_layout(pk, opts, nx, ny, G):
 @pytest.mark.parametrize("cfg,nx,G", [(4, 24, 5), (5, 24, 64), (2, None, None)])
 def test_options_config_recipes(pk, cfg, nx, G):
     prob = synth.config(cfg, nx=nx, G=G) if nx else synth.config(cfg)
-    check(pk, prob, SIG | FIX)
+    check(pk, prob, SIG | FIX | HR)
+
+
+def test_half_range_degenerate_directions(pk):
+    """Directions with Omega_x = 0 or Omega_y = 0 count in the + half (reading R23), as
+    in the sweep's quadrant assignment."""
+    om = np.array([[0.0, 0.6, 0.8], [0.6, 0.0, 0.8], [-0.6, 0.0, -0.8], [0.0, -1.0, 0.0], [0.48, -0.6, 0.64]])
+    w = np.array([0.1, 0.2, 0.3, 0.25, 0.15])
+    prob = random_problem(79, 2, 5, 4, 2, 5, 3, omega=om, w=w)
+    check(pk, prob, HR)
 
 
 def test_fixup_identity_without_negatives(pk):

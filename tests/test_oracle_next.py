@@ -135,3 +135,48 @@ def test_fixup_is_identity_without_negatives():
     fl = np.broadcast_to(Q, (2 * (nx + ny) * 3, G)).copy()
     prob = Problem("c", 2, nx, ny, p, om, w, sig, q, fl, 1.0)
     assert np.array_equal(oracle.sweep(prob), oracle.sweep(prob, opts=FIX))
+
+
+# ------------------------------------------------------------------ NEXT-3
+HR = oracle.HALF_RANGE
+
+
+@pytest.mark.parametrize("dim,p", [(1, 1), (1, 2), (2, 1), (2, 2)])
+def test_half_range_from_independent_psi(dim, p):
+    """F+, P+  = half-range sums of psi from the dense global solve."""
+    nx, ny = (5, 1) if dim == 1 else (3, 2)
+    prob = random_problem(80 + 3 * dim + p, dim, nx, ny, p, 7, 2)
+    f = oracle.unpack(oracle.sweep(prob, opts=HR), dim, nx, ny, p, opts=HR)
+    ref = np.zeros_like(f["HR"])
+    for d in range(prob.n_dir):
+        ox = prob.omega[d, 0]
+        oy = prob.omega[d, 1] if dim == 2 else 0.0
+        w = prob.w[d]
+        rows = [w * ox, w * ox * ox] if dim == 1 else [w * ox, w * oy, w * ox * ox, w * ox * oy, w * oy * oy]
+        for g in range(prob.G):
+            psi = solve_global(prob, d, g)
+            if ox >= 0:
+                for m, c in enumerate(rows):
+                    ref[m] += c * psi
+            if dim == 2 and oy >= 0:
+                for m, c in enumerate(rows):
+                    ref[5 + m] += c * psi
+    assert np.abs(f["HR"] - ref).max() < 1e-13 * np.abs(f["phi"]).max()
+
+
+def test_half_range_isotropic():
+    """psi == Q (constant solution) on a symmetric set: F+_{+x} = Q (alpha_x / 2, 0),
+    P+_{+x} = Q (1/6, 0, 1/6 Oy^2 part), likewise for +y — from sum w Omega Omega = I/3
+    split evenly by the mirror symmetry, and alpha_n = sum w |Omega.n| (eq:alpha)."""
+    nx, ny, p, G = 3, 3, 1, 1
+    om, w = synth.product_set(4, 8)
+    sig = np.full((nx * ny, G), 2.0)
+    q = np.full((nx * ny, 4, G), 3.0)        # sigma~ Q with Q = 1, 1/(c dt) = 1
+    fl = np.ones((2 * (nx + ny) * 2, G))
+    prob = Problem("iso", 2, nx, ny, p, om, w, sig, q, fl, 1.0)
+    f = oracle.unpack(oracle.sweep(prob, opts=HR), 2, nx, ny, p, opts=HR)
+    a = oracle.alpha(prob)
+    Pyy_half = 0.5 * np.sum(w * om[:, 1] ** 2)
+    exp = [a[1] / 2, 0.0, 1 / 6, 0.0, Pyy_half, 0.0, a[3] / 2, np.sum(w * om[:, 0] ** 2) / 2, 0.0, 1 / 6]
+    for m, e in enumerate(exp):
+        assert np.abs(f["HR"][m] - e).max() < 1e-13, (m, f["HR"][m].ravel()[:3], e)
