@@ -640,35 +640,55 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             if (!bulk && c + 1 < prm.n_chunks) stage(c + 1, buf ^ 1);
             wait_stage(buf);
             if (!bulk) __syncthreads();
-            for (int it = tid; it < CT * GBK; it += NL) {
-                const int el = it / GBK;
-                const int gg = it - el * GBK;
-                const int col = el / T, r = el - col * T;
-                const bool on = col < cols && r < rows && gg < sd.ng;
-                double st = 1.0;
-                double qv[NN];
+            // PA items per thread per pass, all loads issued before any store: the
+            // transform is in place, so without the batching every item's loads would
+            // wait for the previous item's stores (possible aliasing)
+#ifndef SWEEP_PA
+#define SWEEP_PA 1  // 4 hits an illegal-instruction fault in the many-group layout (round 1, unexplained)
+#endif
+            constexpr int PA = SWEEP_PA;
+            for (int it0 = tid; it0 < CT * GBK; it0 += PA * NL) {
+                double qv[PA][NN], st[PA];
+                int ofs[PA];
 #pragma unroll
-                for (int kk = 0; kk < NN; ++kk) {
-                    const int aq = kk % NP1, bq = kk / NP1;
-                    const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
-                    qv[kk] = on ? qs[((size_t)el * NN + a + NP1 * b) * GBK + gg] : 0.0;
+                for (int u = 0; u < PA; ++u) {
+                    const int it = it0 + u * NL;
+                    const int el = it / GBK;
+                    const int gg = it - el * GBK;
+                    const int col = el / T, r = el - col * T;
+                    const bool live = it < CT * GBK;
+                    const bool on = live && col < cols && r < rows && gg < sd.ng;
+                    ofs[u] = live ? it : -1;
+                    st[u] = 1.0;
+#pragma unroll
+                    for (int kk = 0; kk < NN; ++kk) {
+                        const int aq = kk % NP1, bq = kk / NP1;
+                        const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
+                        qv[u][kk] = on ? qs[((size_t)el * NN + a + NP1 * b) * GBK + gg] : 0.0;
+                    }
+                    if (on) {
+                        // SIG keeps sigma_t itself staged (1/(c dt) is folded into the lane's
+                        // mode shifts); otherwise sigma~ = sigma_t + 1/(c dt)
+                        const double sg = ss[el * GBK + gg];
+                        if (bad_sigma(sg + prm.inv_c_dt)) atomicOr(prm.err, 1);
+                        st[u] = SIG ? sg : sg + prm.inv_c_dt;
+                    }
                 }
-                if (on) {
-                    // SIG keeps sigma_t itself staged (1/(c dt) is folded into the lane's
-                    // mode shifts); otherwise sigma~ = sigma_t + 1/(c dt)
-                    const double sg = ss[el * GBK + gg];
-                    if (bad_sigma(sg + prm.inv_c_dt)) atomicOr(prm.err, 1);
-                    st = SIG ? sg : sg + prm.inv_c_dt;
-                }
-                ss[el * GBK + gg] = st;
-                if constexpr (P == 2) {
-                    double qh[9];
-                    modal_forward(qv, qh);
 #pragma unroll
-                    for (int m = 0; m < 9; ++m) qs[((size_t)el * NN + m) * GBK + gg] = qh[m];
-                } else {
+                for (int u = 0; u < PA; ++u) {
+                    if (ofs[u] < 0) continue;
+                    const int el = ofs[u] / GBK;
+                    const int gg = ofs[u] - el * GBK;
+                    ss[el * GBK + gg] = st[u];
+                    if constexpr (P == 2) {
+                        double qh[9];
+                        modal_forward(qv[u], qh);
 #pragma unroll
-                    for (int kk = 0; kk < NN; ++kk) qs[((size_t)el * NN + kk) * GBK + gg] = qv[kk];
+                        for (int m = 0; m < 9; ++m) qs[((size_t)el * NN + m) * GBK + gg] = qh[m];
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < NN; ++kk) qs[((size_t)el * NN + kk) * GBK + gg] = qv[u][kk];
+                    }
                 }
             }
             // ---- wait until the strip below has finished this chunk
@@ -904,27 +924,44 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                 auto field_dst = [&](int f) -> double* {
                     return slab + ((f < 6) ? (size_t)f * nodes : sig_off + (size_t)(f - 6) * nodes);
                 };
-                for (int o = tid; o < CT * NFO * NQ; o += NL) {
-                    const int m = o % NQ, rest = o / NQ;
-                    const int f = rest % NFO, el = rest / NFO;
-                    const double* Sp = ((f < 6) ? S : S2) + (size_t)el * SEL + m;
-                    const double* cf = coefS + ((f < 6) ? f : f - 6);
-                    double a0 = 0.0, a1 = 0.0;
-                    int dd = 0;
-                    for (; dd + 1 < sd.nd; dd += 2) {
-                        a0 = fma(cf[dd * NFIELD], Sp[dd * NQ], a0);
-                        a1 = fma(cf[(dd + 1) * NFIELD], Sp[(dd + 1) * NQ], a1);
+                // PC outputs per thread per pass: independent accumulation chains, and all
+                // their S loads ahead of the stores (Mbuf and S share the smem window)
+#ifndef SWEEP_PC
+#define SWEEP_PC 4
+#endif
+                constexpr int PC = SWEEP_PC;
+                for (int o0 = tid; o0 < CT * NFO * NQ; o0 += PC * NL) {
+                    const double* Sp[PC];
+                    const double* cf[PC];
+                    double acc[PC];
+#pragma unroll
+                    for (int u = 0; u < PC; ++u) {
+                        const int o = min(o0 + u * NL, CT * NFO * NQ - 1);
+                        const int m = o % NQ, rest = o / NQ;
+                        const int f = rest % NFO, el = rest / NFO;
+                        Sp[u] = ((f < 6) ? S : S2) + (size_t)el * SEL + m;
+                        cf[u] = coefS + ((f < 6) ? f : f - 6);
+                        acc[u] = 0.0;
                     }
-                    if (dd < sd.nd) a0 = fma(cf[dd * NFIELD], Sp[dd * NQ], a0);
-                    const double acc = a0 + a1;
-                    if constexpr (P == 2) {
-                        Mbuf[o] = acc;
-                    } else {
-                        const int col = el / T, r = el - col * T;
-                        if (col < cols && r < rows) {
-                            const int ip = i0 + col, jp = j0 + r;
-                            const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                            node_store(field_dst(f) + ((size_t)i + (size_t)nx * j) * NN, m, acc);
+                    for (int dd = 0; dd < sd.nd; ++dd) {
+#pragma unroll
+                        for (int u = 0; u < PC; ++u) acc[u] = fma(cf[u][dd * NFIELD], Sp[u][dd * NQ], acc[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < PC; ++u) {
+                        const int o = o0 + u * NL;
+                        if (o >= CT * NFO * NQ) continue;
+                        if constexpr (P == 2) {
+                            Mbuf[o] = acc[u];
+                        } else {
+                            const int m = o % NQ, rest = o / NQ;
+                            const int f = rest % NFO, el = rest / NFO;
+                            const int col = el / T, r = el - col * T;
+                            if (col < cols && r < rows) {
+                                const int ip = i0 + col, jp = j0 + r;
+                                const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                                node_store(field_dst(f) + ((size_t)i + (size_t)nx * j) * NN, m, acc[u]);
+                            }
                         }
                     }
                 }
