@@ -52,6 +52,14 @@ def _load():
         lib.oracle_out_size2.restype = i
         lib.oracle_fixup.argtypes = [i, dp, dp]
         lib.oracle_fixup.restype = i
+        lib.oracle_planck_P.argtypes = [d]
+        lib.oracle_planck_P.restype = d
+        lib.oracle_planck_groups.argtypes = [d, i, dp, dp]
+        lib.oracle_planck_groups.restype = None
+        lib.oracle_t_eliminate.argtypes = [d, d, i, dp, dp, d]
+        lib.oracle_t_eliminate.restype = d
+        lib.oracle_trt_step.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, dp, dp, dp, dp, d, d, d, i, dp, i]
+        lib.oracle_trt_step.restype = i
         lib.oracle_sweep_psi.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, i, i, dp, i]
         lib.oracle_sweep_psi.restype = i
         lib.oracle_alpha.argtypes = [i, i, dp, dp, dp]
@@ -98,6 +106,41 @@ def fixup(x, W) -> np.ndarray:
     x, W = _c(np.array(x, dtype=np.float64)), _c(W)
     lib.oracle_fixup(x.size, _ptr(W), _ptr(x))
     return x
+
+
+def planck_P(x: float) -> float:
+    """(15/pi^4) int_0^x t^3/(e^t-1) dt by composite Gauss-Legendre quadrature."""
+    return _load().oracle_planck_P(float(x))
+
+
+def planck_groups(T: float, nu) -> np.ndarray:
+    """B_g(T) = T^4 [P(nu_{g+1}/T) - P(nu_g/T)] for the bounds nu[0..G] (a = c = 1)."""
+    nu = _c(nu)
+    out = np.zeros(nu.size - 1)
+    _load().oracle_planck_groups(float(T), nu.size - 1, _ptr(nu), _ptr(out))
+    return out
+
+
+def t_eliminate(Tk: float, sphi: float, sigma_g, nu, cv_dt: float) -> float:
+    """Root T of cv/dt (T - Tk) + sum_g sigma_g B_g(T) = sphi, by bisection."""
+    s, nu = _c(sigma_g), _c(nu)
+    return _load().oracle_t_eliminate(float(Tk), float(sphi), s.size, _ptr(s), _ptr(nu), float(cv_dt))
+
+
+def trt_step(prob, Tk, Iprev, nu, cv: float, dt: float, eps: float = 1e-4, max_iter: int = 50,
+             nthreads: int = 0):
+    """One unaccelerated backward-Euler TRT step (NEXT-4).  prob supplies mesh, quadrature,
+    sigma [N_el][G] and inflow; Tk [N_el][n], Iprev [N_el][n][G].  Returns (T, iterations)."""
+    lib = _load()
+    om, w, s, fl = _c(prob.omega), _c(prob.w), _c(prob.sigma), _c(prob.inflow)
+    Tk, Ip, nu = _c(Tk), _c(Iprev), _c(nu)
+    T = np.zeros_like(Tk)
+    rc = lib.oracle_trt_step(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
+                             s.shape[1], _ptr(s), _ptr(fl), _ptr(Tk), _ptr(Ip), _ptr(nu), float(cv), float(dt),
+                             float(eps), int(max_iter), _ptr(T), int(nthreads))
+    if rc < 0:
+        raise RuntimeError(f"oracle_trt_step failed rc={rc}")
+    return T, rc
 
 
 def sweep_psi(prob, d: int, g: int, opts: int = 0) -> np.ndarray:

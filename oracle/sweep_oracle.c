@@ -37,6 +37,16 @@
  *       F+_n = sum_g sum_{Omega.n > 0} w Omega psi,  P+_n = sum_g sum_{Omega.n > 0} w Omega Omega psi
  *   for n = +x, +y (dim 1: n = +x), with Omega.n = 0 counted as + (reading R23).
  *
+ * oracle_trt_step: one backward-Euler step of the UNACCELERATED
+ * scheme: repeat { emission source q_g = sigma_g B_g(T) + I^k_g/dt
+ * from the current temperature (eq:smm_be_transport; c = 1); sweep;
+ * pointwise nonlinear elimination of T from the energy balance
+ *     C_v (T - T^k)/dt = sum_g sigma_g (phi_g - B_g(T))   (eq:smm_be_meb)
+ * } until ||T^{l+1} - T^l||_2 <= eps ||T^{l+1}||_2 (eq:relative_tol).
+ * B_g(T) = T^4 [P(nu_{g+1}/T) - P(nu_g/T)], P(x) = (15/pi^4) int_0^x t^3/(e^t-1) dt
+ * (eq:planck PAPER.md:106-125, a = c = 1) evaluated here by composite Gauss-Legendre
+ * quadrature of the integrand (no series), and T found by bisection (no Newton).
+ *
  * How (deliberately plain): for each (d,g), elements are visited in upwind
  * nested-loop order; the element matrix is assembled UNSCALED straight from
  * the weak form and solved with partial-pivot LU; contributions are summed
@@ -52,6 +62,7 @@
  * jump/average form, closed-form 1-D transmission, constant-solution
  * exactness, particle balance, convergence order, symmetries).
  */
+#define _GNU_SOURCE
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -514,4 +525,145 @@ int oracle_sweep(int dim, int nx, int ny, double lx, double ly, int p, int ndir,
                  double inv_c_dt, const double *q, const double *inflow, double *out,
                  int nthreads) {
     return oracle_sweep2(dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, inv_c_dt, q, inflow, out, nthreads, 0);
+}
+
+/* ---------------------------------------------------------------- NEXT-4 */
+/* 20-point Gauss-Legendre rule on [-1,1], nodes found by Newton on P_20 */
+static double gl_x[20], gl_w[20];
+static int gl_ready = 0;
+static void gl_init(void) {
+    if (gl_ready) return;
+    const int n = 20;
+    for (int i = 0; i < n; ++i) {
+        double x = cos(M_PI * (i + 0.75) / (n + 0.5));
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = x;
+            for (int k = 2; k <= n; ++k) {
+                double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            double dp = n * (x * p1 - p0) / (x * x - 1.0);
+            double dx = p1 / dp;
+            x -= dx;
+            if (fabs(dx) < 1e-16) {
+                p0 = 1.0; p1 = x;
+                for (int k = 2; k <= n; ++k) {
+                    double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+                    p0 = p1;
+                    p1 = p2;
+                }
+                dp = n * (x * p1 - p0) / (x * x - 1.0);
+                break;
+            }
+        }
+        gl_x[i] = x;
+        double p0 = 1.0, p1 = x;
+        for (int k = 2; k <= n; ++k) {
+            double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+            p0 = p1;
+            p1 = p2;
+        }
+        double dp = n * (x * p1 - p0) / (x * x - 1.0);
+        gl_w[i] = 2.0 / ((1.0 - x * x) * dp * dp);
+    }
+    gl_ready = 1;
+}
+
+static double planck_integrand(double t) { return (t < 1e-300) ? 0.0 : t * t * t / expm1(t); }
+
+/* P(x) = (15/pi^4) int_0^x t^3/(e^t-1) dt, composite 20-point Gauss-Legendre on unit
+ * panels up to min(x, 60) (the tail beyond 60 is < 1e-20 of the total). */
+double oracle_planck_P(double x) {
+    if (!(x > 0.0)) return 0.0;
+    gl_init();
+    const double X = (x < 60.0) ? x : 60.0;
+    const int np = (int)ceil(X);
+    double s = 0.0;
+    for (int k = 0; k < np; ++k) {
+        const double a = X * k / np, b = X * (k + 1) / np, m = 0.5 * (a + b), hw = 0.5 * (b - a);
+        double ps = 0.0;
+        for (int i = 0; i < 20; ++i) ps += gl_w[i] * planck_integrand(m + hw * gl_x[i]);
+        s += hw * ps;
+    }
+    return s * 15.0 / (M_PI * M_PI * M_PI * M_PI);
+}
+
+/* B_g(T) for g = 0..G-1 from the bounds nu[0..G] */
+static void planck_groups_T(double T, int G, const double *nu, double *Bg) {
+    const double T4 = T * T * T * T;
+    double Pl = oracle_planck_P(nu[0] / T);
+    for (int g = 0; g < G; ++g) {
+        const double Pr = oracle_planck_P(nu[g + 1] / T);
+        Bg[g] = T4 * (Pr - Pl);
+        Pl = Pr;
+    }
+}
+
+void oracle_planck_groups(double T, int G, const double *nu, double *Bg) { planck_groups_T(T, G, nu, Bg); }
+
+/* nonlinear elimination at one node: f(T) = cv/dt (T - Tk) + sum_g sig_g B_g(T) - sphi = 0,
+ * f increasing in T >= 0; bisection to relative width 1e-15 */
+double oracle_t_eliminate(double Tk, double sphi, int G, const double *sig, const double *nu, double cv_dt) {
+    double Bg[512];
+    if (G > 512) return -1.0;
+    #define F_OF(T, out) do { planck_groups_T((T), G, nu, Bg); double e_ = 0.0; \
+        for (int g_ = 0; g_ < G; ++g_) e_ += sig[g_] * Bg[g_]; (out) = cv_dt * ((T) - Tk) + e_ - sphi; } while (0)
+    double lo = 0.0, hi = (Tk > 1.0) ? Tk : 1.0, fh;
+    F_OF(hi, fh);
+    while (fh < 0.0) { lo = hi; hi *= 2.0; F_OF(hi, fh); }
+    while (hi - lo > 1e-15 * hi) {
+        const double mid = 0.5 * (lo + hi);
+        double fm;
+        F_OF(mid, fm);
+        if (fm < 0.0) lo = mid; else hi = mid;
+        if (mid == lo && mid == hi) break;
+    }
+    #undef F_OF
+    return 0.5 * (lo + hi);
+}
+
+/* One unaccelerated backward-Euler step.  Tk, T [N_el][n] nodal; Iprev [N_el][n][G]
+ * isotropic previous intensity; sigma [N_el][G]; inflow [N_bnode][G]; nu [G+1].
+ * c = 1: 1/(c dt) = 1/dt.  Runs until the relative 2-norm change is <= eps (eps > 0)
+ * or max_iter iterations; returns the iteration count, or < 0 on failure. */
+int oracle_trt_step(int dim, int nx, int ny, double lx, double ly, int p, int ndir, const double *omega,
+                    const double *w, int G, const double *sigma, const double *inflow, const double *Tk,
+                    const double *Iprev, const double *nu, double cv, double dt, double eps, int max_iter,
+                    double *T, int nthreads) {
+    prob P;
+    int rc = setup(&P, dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, 1.0 / dt, Iprev, inflow);
+    if (rc) return rc;
+    size_t nodes;
+    int nT;
+    const size_t nout = out_size(&P, &nodes, &nT, 1);
+    const size_t off_sig = (size_t)(1 + dim + nT) * nodes + 2 * (size_t)P.nbnode;
+    double *q = (double *)malloc(sizeof(double) * nodes * G);
+    double *out = (double *)malloc(sizeof(double) * nout);
+    double *Tn = (double *)malloc(sizeof(double) * nodes);
+    double *Bg = (double *)malloc(sizeof(double) * G);
+    if (!q || !out || !Tn || !Bg) { free(q); free(out); free(Tn); free(Bg); return -3; }
+    for (size_t v = 0; v < nodes; ++v) T[v] = Tk[v];
+    int it = 0;
+    for (it = 1; it <= max_iter; ++it) {
+        for (size_t v = 0; v < nodes; ++v) {
+            const size_t e = v / P.n;
+            planck_groups_T(T[v], G, nu, Bg);
+            for (int g = 0; g < G; ++g) q[v * G + g] = sigma[e * G + g] * Bg[g] + Iprev[v * G + g] / dt;
+        }
+        rc = oracle_sweep2(dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, 1.0 / dt, q, inflow, out, nthreads, 1);
+        if (rc) break;
+        double dn = 0.0, tn = 0.0;
+        for (size_t v = 0; v < nodes; ++v) {
+            const size_t e = v / P.n;
+            Tn[v] = oracle_t_eliminate(Tk[v], out[off_sig + v], G, sigma + e * G, nu, cv / dt);
+            dn += (Tn[v] - T[v]) * (Tn[v] - T[v]);
+            tn += Tn[v] * Tn[v];
+        }
+        for (size_t v = 0; v < nodes; ++v) T[v] = Tn[v];
+        if (eps > 0.0 && sqrt(dn) <= eps * sqrt(tn)) break;
+    }
+    if (it > max_iter) it = max_iter;
+    free(q); free(out); free(Tn); free(Bg);
+    return rc ? rc : it;
 }

@@ -180,3 +180,128 @@ def test_half_range_isotropic():
     exp = [a[1] / 2, 0.0, 1 / 6, 0.0, Pyy_half, 0.0, a[3] / 2, np.sum(w * om[:, 0] ** 2) / 2, 0.0, 1 / 6]
     for m, e in enumerate(exp):
         assert np.abs(f["HR"][m] - e).max() < 1e-13, (m, f["HR"][m].ravel()[:3], e)
+
+
+# ------------------------------------------------------------------ NEXT-4
+def _bern_series_P(x):
+    """(15/pi^4) int_0^x t^3/(e^t-1) dt by the Bernoulli series (|x| < 2 pi) — a second
+    formula for the quadrature the oracle uses."""
+    import math
+    B = {0: 1.0, 1: -0.5, 2: 1 / 6, 4: -1 / 30, 6: 1 / 42, 8: -1 / 30, 10: 5 / 66, 12: -691 / 2730, 14: 7 / 6,
+         16: -3617 / 510, 18: 43867 / 798, 20: -174611 / 330, 22: 854513 / 138, 24: -236364091 / 2730}
+    s = sum(b * x ** (k + 3) / (math.factorial(k) * (k + 3)) for k, b in B.items())
+    return s * 15 / math.pi ** 4
+
+
+def test_planck_integral_pins():
+    """P(inf) = 1 (int_0^inf t^3/(e^t-1) = pi^4/15); small-x limit; Bernoulli series."""
+    import math
+    assert abs(oracle.planck_P(1e4) - 1.0) < 1e-15
+    x = 1e-3
+    assert abs(oracle.planck_P(x) / (15 / math.pi ** 4 * x ** 3 / 3) - 1.0) < 1e-3
+    for x in (0.05, 0.5, 1.0, 1.5):
+        assert abs(oracle.planck_P(x) - _bern_series_P(x)) < 2e-15, x
+    # large x: 1 - (15/pi^4) sum_n e^{-n x} (x^3/n + 3x^2/n^2 + 6x/n^3 + 6/n^4)
+    for x in (2.0, 3.0, 5.0, 12.0, 40.0):
+        tail = sum(math.exp(-n * x) * (x ** 3 / n + 3 * x ** 2 / n ** 2 + 6 * x / n ** 3 + 6 / n ** 4)
+                   for n in range(1, 60))
+        assert abs(oracle.planck_P(x) - (1 - 15 / math.pi ** 4 * tail)) < 2e-15, x
+
+
+def test_stefan_boltzmann():
+    """sum_g B_g(T) over bounds covering (0, inf) = T^4 (a = c = 1)."""
+    nu = np.concatenate([[0.0], np.logspace(-3, 4, 40)])
+    for T in (0.05, 1.0, 7.0):
+        assert abs(oracle.planck_groups(T, nu).sum() / T ** 4 - 1.0) < 1e-13
+
+
+def test_t_elimination_pins():
+    """Fixed point (sphi = sum sigma B_g(Tk) => T = Tk), the residual of the root, and
+    the heat-capacity-dominated limit T = Tk + (sphi - sum sigma B(Tk)) / (cv/dt + sum sigma B')."""
+    nu = synth.planck.group_bounds(6)
+    sig = np.array([3.0, 1.0, 0.5, 20.0, 7.0, 0.1])
+    Tk = 0.7
+    e0 = float(sig @ oracle.planck_groups(Tk, nu))
+    assert abs(oracle.t_eliminate(Tk, e0, sig, nu, 5.0) - Tk) < 1e-14
+    T = oracle.t_eliminate(Tk, 2.0 * e0, sig, nu, 5.0)
+    res = 5.0 * (T - Tk) + sig @ oracle.planck_groups(T, nu) - 2.0 * e0
+    assert abs(res) < 1e-13 * 2.0 * e0
+    big = 1e5
+    T = oracle.t_eliminate(Tk, e0 + 1e-3, sig, nu, big)
+    h = 1e-5
+    dE = (sig @ oracle.planck_groups(Tk + h, nu) - sig @ oracle.planck_groups(Tk - h, nu)) / (2 * h)
+    assert abs((T - Tk) * (big + dE) / 1e-3 - 1.0) < 1e-6   # linearised update
+
+
+def _trt_problem(dim, p, nx, ny, G, seed=5):
+    om, w = synth.slab_set(4) if dim == 1 else synth.product_set(2, 8)
+    rng = np.random.default_rng(seed)
+    nu = synth.planck.group_bounds(G)
+    ne = nx * (ny if dim == 2 else 1)
+    n = (p + 1) ** dim
+    sig = np.exp(rng.uniform(np.log(0.5), np.log(40.0), size=(ne, G)))
+    nb = 2 if dim == 1 else 2 * (nx + ny) * (p + 1)
+    Tb = 1.0
+    inflow = np.broadcast_to(oracle.planck_groups(Tb, nu), (nb, G)).copy()
+    Tk = rng.uniform(0.3, 0.9, size=(ne, n))
+    Iprev = np.stack([np.stack([oracle.planck_groups(t, nu) for t in row]) for row in Tk])
+    prob = Problem("trt", dim, nx, ny if dim == 2 else 1, p, om, w, sig, np.zeros((ne, n, G)), inflow, 1.0)
+    return prob, Tk, Iprev, nu
+
+
+def test_trt_step_equilibrium():
+    """Uniform equilibrium (T = T0 everywhere, I^k = inflow = B_g(T0)) is a fixed point:
+    one iteration, T = T0."""
+    prob, Tk, Iprev, nu = _trt_problem(2, 1, 3, 3, 4)
+    T0 = 0.8
+    Tk[:] = T0
+    Iprev[:] = oracle.planck_groups(T0, nu)
+    prob.inflow[:] = oracle.planck_groups(T0, nu)
+    T, it = oracle.trt_step(prob, Tk, Iprev, nu, cv=0.3, dt=0.05, eps=1e-12, max_iter=5)
+    assert np.abs(T - T0).max() < 1e-13 and it == 1
+
+
+@pytest.mark.parametrize("dim,p", [(1, 1), (2, 1)])
+def test_trt_step_fixed_point_brute_force(dim, p):
+    """The converged step is the fixed point T = elim(sweep(q(T))); an independent solve:
+    Newton on the full nodal vector with psi from the dense global DG solve
+    (tests/dense_dg.py) and a finite-difference Jacobian."""
+    nx, ny, G = (3, 1, 3) if dim == 1 else (2, 2, 2)
+    prob, Tk, Iprev, nu = _trt_problem(dim, p, nx, ny, G)
+    cv, dt = 0.4, 0.02
+    T_or, it = oracle.trt_step(prob, Tk, Iprev, nu, cv=cv, dt=dt, eps=1e-14, max_iter=200)
+    assert it < 200
+    ne, n = Tk.shape
+
+    def residual(Tv):
+        Tn = Tv.reshape(ne, n)
+        q = np.zeros((ne, n, G))
+        for e in range(ne):
+            for k in range(n):
+                q[e, k] = prob.sigma[e] * oracle.planck_groups(Tn[e, k], nu) + Iprev[e, k] / dt
+        pr = Problem("fp", prob.dim, prob.nx, prob.ny, p, prob.omega, prob.w, prob.sigma, q, prob.inflow, 1.0 / dt)
+        phi = np.zeros((ne, n, G))
+        for d in range(pr.n_dir):
+            for g in range(G):
+                phi[:, :, g] += pr.w[d] * solve_global(pr, d, g)
+        r = np.zeros((ne, n))
+        for e in range(ne):
+            for k in range(n):
+                r[e, k] = (cv / dt * (Tn[e, k] - Tk[e, k]) + prob.sigma[e] @ oracle.planck_groups(Tn[e, k], nu)
+                           - prob.sigma[e] @ phi[e, k])
+        return r.ravel()
+
+    Tv = Tk.ravel().copy()
+    for _ in range(30):
+        r = residual(Tv)
+        Jm = np.zeros((Tv.size, Tv.size))
+        for i in range(Tv.size):
+            h = 1e-7 * Tv[i]
+            Tp = Tv.copy()
+            Tp[i] += h
+            Jm[:, i] = (residual(Tp) - r) / h
+        step = np.linalg.solve(Jm, -r)
+        Tv += step
+        if np.abs(step).max() < 1e-15 * Tv.max():
+            break
+    assert np.abs(T_or.ravel() - Tv).max() < 1e-12 * Tv.max()
