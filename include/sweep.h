@@ -142,6 +142,35 @@ int closures_get(sweep_handle *h, double *out, size_t n_doubles, void *cuda_stre
 int sweep_run_host(sweep_handle *h, const double *h_sigma, double inv_c_dt, const double *h_q,
                    const double *h_inflow, double *h_out, size_t n_doubles, void *cuda_stream);
 
+/* One backward-Euler step of the UNACCELERATED TRT scheme (
+ * SURVEY NEXT-4), the baseline the SM acceleration is measured against:
+ *   repeat {  q_g = sigma_g B_g(T) + I^k_g / dt            (emission, eq:smm_be_transport, c = 1)
+ *             sweep_run(sigma, 1/dt, q, inflow)           (this handle)
+ *             T <- root of C_v (T - T^k)/dt + sum_g sigma_g B_g(T) = sum_g sigma_g phi_g
+ *                  at every node (pointwise nonlinear elimination, PAPER.md:588-596;
+ *                  bracketed Newton to 1e-15 relative)
+ *   } until ||T_new - T||_2 <= eps ||T_new||_2 (eq:relative_tol; paper: eps = 1e-4 for this
+ *   scheme) or max_iter iterations.
+ * B_g(T) = T^4 [P(nu_{g+1}/T) - P(nu_g/T)], P the normalised Planck integral (a = c = 1).
+ * Requires a handle set up with SWEEP_SIGMA_MOMENTS and nranks = 1.
+ *   d_sigma [N_el][G], d_inflow [N_bnode][G]  as for sweep_run (sigma at T^k: explicit)
+ *   d_Tk    [N_el][n]     nodal temperature at t_k (> 0)
+ *   d_Iprev [N_el][n][G]  isotropic intensity at t_k (the time-edge source, reading R17)
+ *   d_T     [N_el][n]     output: T^{k+1} (may alias nothing else)
+ * *iterations receives the number of outer iterations (sweeps) run.  The gray outputs
+ * of the last sweep stay available through closures_get.  Errors: SWEEP_E_ARG (flags,
+ * ranks, parameters), SWEEP_E_SIGMA (device flags, incl. a failed elimination). */
+typedef struct {
+    const double *nu;   /* HOST [G_loc + 1] group bounds, increasing, >= 0 (temperature units) */
+    double cv;          /* volumetric heat capacity C_v > 0 */
+    double dt;          /* time step > 0 */
+    double eps;         /* relative tolerance of the outer iteration; <= 0: run max_iter */
+    int max_iter;       /* >= 1 */
+} trt_params;
+
+int trt_step(sweep_handle *h, const double *d_sigma, const double *d_inflow, const double *d_Tk,
+             const double *d_Iprev, const trt_params *prm, double *d_T, int *iterations, void *cuda_stream);
+
 /* Statistics of the last sweep_run: number of kernels launched (out[0]),
  * distinct directions swept (out[1], after folding), work streams (out[2]),
  * persistent CTAs (out[3]). */

@@ -1,0 +1,187 @@
+// k_trt.cu — the UNACCELERATED TRT iteration around the sweep (
+// PAPER.md:667-672): emission source from the current temperature, and the pointwise
+// nonlinear elimination of the temperature from the energy balance
+//     C_v (T - T^k)/dt + sum_g sigma_g B_g(T) = sum_g sigma_g phi_g   (eq:smm_be_meb, c = 1)
+// with sum_g sigma_g phi_g the sweep's sigma-weighted moment (SWEEP_SIGMA_MOMENTS).
+// B_g(T) = T^4 [P(nu_{g+1}/T) - P(nu_g/T)], P(x) = (15/pi^4) int_0^x t^3/(e^t-1) dt
+// (eq:planck PAPER.md:106-125, a = c = 1), evaluated with the two classical series of
+// the Planck integral ("polylogarithmic and Taylor series expansions").
+#include <cuda_runtime.h>
+
+#include "sweep_internal.h"
+
+namespace sweepk {
+
+constexpr double K15_PI4 = 0.15398973382026503;  // 15 / pi^4
+
+// int_0^x t^3/(e^t-1) dt * 15/pi^4 and its derivative (15/pi^4) x^3/(e^x-1)
+__device__ __forceinline__ void planck_P(double x, double& P, double& dP) {
+    if (!(x > 0.0)) {
+        P = 0.0;
+        dP = 0.0;
+        return;
+    }
+    const double x2 = x * x, x3 = x2 * x;
+    dP = K15_PI4 * x3 / expm1(x);
+    if (x < 1.5) {
+        // Bernoulli series sum_k B_k x^(k+3) / (k! (k+3)) (|x| < 2 pi): x^3/3 - x^4/8 +
+        // sum_j c_j x^(2j+3), c_j = B_2j / ((2j)! (2j+3)), j = 1..12 (Horner in x^2)
+        const double c[13] = {1.0 / 3.0,
+                              1.0 / 60.0,                    // B2/(2! 5)
+                              -1.0 / 5040.0,                 // B4/(4! 7)
+                              1.0 / 272160.0,                // B6/(6! 9)
+                              -1.0 / 13305600.0,             // B8/(8! 11)
+                              1.0 / 622702080.0,             // B10/(10! 13)
+                              -691.0 / (2730.0 * 479001600.0 * 15.0),
+                              7.0 / (6.0 * 87178291200.0 * 17.0),
+                              -3617.0 / (510.0 * 20922789888000.0 * 19.0),
+                              43867.0 / (798.0 * 6402373705728000.0 * 21.0),
+                              -174611.0 / (330.0 * 2432902008176640000.0 * 23.0),
+                              854513.0 / (138.0 * 1.1240007277776077e21 * 25.0),
+                              -236364091.0 / (2730.0 * 6.204484017332394e23 * 27.0)};
+        double s = c[12];
+#pragma unroll
+        for (int j = 11; j >= 1; --j) s = fma(s, x2, c[j]);
+        // sum = x^3 [1/3 - x/8 + x^2 (c1 + x^2 (c2 + ...))]
+        const double even = fma(s, x2, 0.0);
+        P = K15_PI4 * x3 * (c[0] - x * 0.125 + even);
+    } else {
+        // 1 - (15/pi^4) sum_n e^{-n x} (x^3/n + 3x^2/n^2 + 6x/n^3 + 6/n^4)
+        double tail = 0.0;
+        const double e1 = exp(-x);
+        double en = 1.0;
+        const int nmax = (int)(38.0 / x) + 2;
+        for (int n = 1; n <= nmax; ++n) {
+            en *= e1;
+            const double rn = 1.0 / n;
+            tail += en * rn * (x3 + rn * (3.0 * x2 + rn * (6.0 * x + 6.0 * rn)));
+        }
+        P = 1.0 - K15_PI4 * tail;
+    }
+}
+
+// sum_g sig_g B_g(T) and its T-derivative, nu[0..G]
+__device__ __forceinline__ void emission_sum(double T, int G, const double* __restrict__ sig,
+                                             const double* __restrict__ nu, double& E, double& dE) {
+    const double T3 = T * T * T, T4 = T3 * T, iT = 1.0 / T;
+    double Pl, dPl;
+    double xl = nu[0] * iT;
+    planck_P(xl, Pl, dPl);
+    E = 0.0;
+    dE = 0.0;
+    for (int g = 0; g < G; ++g) {
+        const double xr = nu[g + 1] * iT;
+        double Pr, dPr;
+        planck_P(xr, Pr, dPr);
+        const double s = sig[g];
+        E = fma(s, T4 * (Pr - Pl), E);
+        // dB/dT = 4 T^3 (Pr - Pl) - T^3 (xr P'(xr) - xl P'(xl))
+        dE = fma(s, T3 * (4.0 * (Pr - Pl) - (xr * dPr - xl * dPl)), dE);
+        Pl = Pr;
+        dPl = dPr;
+        xl = xr;
+    }
+}
+
+// q[v][g] = sigma[e][g] B_g(T[v]) + Iprev[v][g] * inv_dt   (v = e*n + k)
+__global__ void trt_emission_kernel(const double* __restrict__ T, const double* __restrict__ sigma,
+                                    const double* __restrict__ Iprev, const double* __restrict__ nu, int G, int n,
+                                    size_t nodes, double inv_dt, double* __restrict__ q) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nodes * G; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t v = i / G;
+        const int g = (int)(i - v * G);
+        const size_t e = v / n;
+        const double t = T[v];
+        double Pl, Pr, d;
+        planck_P(nu[g] / t, Pl, d);
+        planck_P(nu[g + 1] / t, Pr, d);
+        const double t2 = t * t;
+        q[i] = fma(sigma[e * G + g], t2 * t2 * (Pr - Pl), Iprev[i] * inv_dt);
+    }
+}
+
+// per node: solve cv_dt (T - Tk) + E(T) = sphi by bracketed Newton from the current
+// iterate T; writes the new T and per-block partial sums of (dT^2, T^2) for the
+// convergence test (summed in a fixed order afterwards: deterministic)
+__global__ void __launch_bounds__(256) trt_update_kernel(const double* __restrict__ Tk, double* __restrict__ T,
+                                                         const double* __restrict__ sphi, const double* __restrict__ sigma,
+                                                         const double* __restrict__ nu, int G, int n, size_t nodes,
+                                                         double cv_dt, double* __restrict__ partial, int* err) {
+    __shared__ double red[2][256];
+    double dsq = 0.0, tsq = 0.0;
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += (size_t)gridDim.x * blockDim.x) {
+        const double* sg = sigma + (v / n) * G;
+        const double tk = Tk[v], s = sphi[v], told = T[v];
+        double t = told > 0.0 ? told : (tk > 0.0 ? tk : 1.0);
+        double lo = 0.0, hi = -1.0;  // hi < 0: no upper bracket yet
+        bool ok = false;
+        for (int it = 0; it < 100; ++it) {
+            double E, dE;
+            emission_sum(t, G, sg, nu, E, dE);
+            const double f = fma(cv_dt, t - tk, E - s);
+            if (f == 0.0) {
+                ok = true;
+                break;
+            }
+            if (f < 0.0) lo = t;
+            else hi = t;
+            double tn = t - f / (cv_dt + dE);
+            if (!(tn > lo) || (hi > 0.0 && !(tn < hi))) tn = (hi > 0.0) ? 0.5 * (lo + hi) : 2.0 * t;
+            const bool done = fabs(tn - t) <= 1e-15 * tn;
+            t = tn;
+            if (done) {
+                ok = true;
+                break;
+            }
+        }
+        if (!ok || !(t > 0.0) || !(t < 1e300)) atomicOr(err, 16);
+        T[v] = t;
+        dsq = fma(t - told, t - told, dsq);
+        tsq = fma(t, t, tsq);
+    }
+    red[0][threadIdx.x] = dsq;
+    red[1][threadIdx.x] = tsq;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + w];
+            red[1][threadIdx.x] += red[1][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = red[0][0];
+        partial[2 * blockIdx.x + 1] = red[1][0];
+    }
+}
+
+// fixed-order sum of the per-block partials -> out[2] (one thread: tiny)
+__global__ void trt_norm_kernel(const double* __restrict__ partial, int nblocks, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < nblocks; ++i) {
+            a += partial[2 * i];
+            b += partial[2 * i + 1];
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+int trt_blocks() { return 148 * 4; }
+
+int launch_trt_emission(const double* T, const double* sigma, const double* Iprev, const double* nu, int G, int n,
+                        size_t nodes, double inv_dt, double* q, void* stream) {
+    trt_emission_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(T, sigma, Iprev, nu, G, n, nodes, inv_dt, q);
+    return (int)cudaGetLastError();
+}
+
+int launch_trt_update(const double* Tk, double* T, const double* sphi, const double* sigma, const double* nu, int G,
+                      int n, size_t nodes, double cv_dt, double* partial, double* norms, int* err, void* stream) {
+    const int nb = trt_blocks();
+    trt_update_kernel<<<nb, 256, 0, (cudaStream_t)stream>>>(Tk, T, sphi, sigma, nu, G, n, nodes, cv_dt, partial, err);
+    trt_norm_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(partial, nb, norms);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace sweepk

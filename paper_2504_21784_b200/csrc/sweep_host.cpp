@@ -109,6 +109,9 @@ struct sweep_handle {
     size_t progress_ints = 0;
     // host-API staging
     double *d_in_sigma = nullptr, *d_in_q = nullptr, *d_in_inflow = nullptr;
+    // unaccelerated TRT iteration workspace (trt_step)
+    double *d_trt_q = nullptr, *d_trt_nu = nullptr, *d_trt_part = nullptr, *d_trt_norm = nullptr;
+    int trt_nu_len = 0;
     ncclComm_t comm = nullptr;
     long long launches = 0;
     // timing ring
@@ -759,6 +762,60 @@ extern "C" int sweep_run_host(sweep_handle* h, const double* h_sigma, double inv
     return closures_get(h, h_out, n, stream);
 }
 
+extern "C" int trt_step(sweep_handle* h, const double* d_sigma, const double* d_inflow, const double* d_Tk,
+                        const double* d_Iprev, const trt_params* prm, double* d_T, int* iterations, void* stream) {
+    if (!h || !d_sigma || !d_inflow || !d_Tk || !d_Iprev || !prm || !prm->nu || !d_T || !iterations)
+        return SWEEP_E_ARG;
+    if (!(h->opt & sweepk::OPT_SIGMA)) return fail(h, SWEEP_E_ARG, "trt_step needs a handle with SWEEP_SIGMA_MOMENTS");
+    if (h->nranks != 1) return fail(h, SWEEP_E_ARG, "trt_step runs on one rank (the elimination needs every group)");
+    if (!(prm->cv > 0) || !(prm->dt > 0) || prm->max_iter < 1 || !std::isfinite(prm->cv) || !std::isfinite(prm->dt))
+        return fail(h, SWEEP_E_ARG, "trt_step: cv, dt > 0 and max_iter >= 1 required");
+    for (int g = 0; g <= h->G; ++g)
+        if (!(prm->nu[g] >= 0) || (g > 0 && !(prm->nu[g] > prm->nu[g - 1])))
+            return fail(h, SWEEP_E_ARG, "trt_step: nu must be increasing and >= 0");
+    DeviceGuard guard(h->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t ce;
+    const size_t nq = h->nodes * (size_t)h->G;
+    if (!h->d_trt_q) {
+        if ((ce = cudaMalloc(&h->d_trt_q, sizeof(double) * nq))) return cuda_fail(h, ce, "cudaMalloc trt q");
+        if ((ce = cudaMalloc(&h->d_trt_nu, sizeof(double) * (h->G + 1)))) return cuda_fail(h, ce, "cudaMalloc trt nu");
+        if ((ce = cudaMalloc(&h->d_trt_part, sizeof(double) * 2 * sweepk::trt_blocks())))
+            return cuda_fail(h, ce, "cudaMalloc trt partials");
+        if ((ce = cudaMalloc(&h->d_trt_norm, sizeof(double) * 2))) return cuda_fail(h, ce, "cudaMalloc trt norms");
+    }
+    if ((ce = cudaMemcpyAsync(h->d_trt_nu, prm->nu, sizeof(double) * (h->G + 1), cudaMemcpyHostToDevice, st)))
+        return cuda_fail(h, ce, "copy nu");
+    if ((ce = cudaMemcpyAsync(d_T, d_Tk, sizeof(double) * h->nodes, cudaMemcpyDeviceToDevice, st)))
+        return cuda_fail(h, ce, "copy Tk");
+    const double inv_dt = 1.0 / prm->dt, cv_dt = prm->cv / prm->dt;
+    int it = 0;
+    for (it = 1; it <= prm->max_iter; ++it) {
+        int e = sweepk::launch_trt_emission(d_T, d_sigma, d_Iprev, h->d_trt_nu, h->G, h->n, h->nodes, inv_dt, h->d_trt_q,
+                                            stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "launch trt emission");
+        int rc = sweep_run(h, d_sigma, inv_dt, h->d_trt_q, d_inflow, stream);
+        if (rc) return rc;
+        e = sweepk::launch_trt_update(d_Tk, d_T, h->d_out + h->off[5], d_sigma, h->d_trt_nu, h->G, h->n, h->nodes, cv_dt,
+                                      h->d_trt_part, h->d_trt_norm, h->d_err, stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "launch trt update");
+        double norms[2] = {0.0, 0.0};
+        if ((ce = cudaMemcpyAsync(norms, h->d_trt_norm, sizeof norms, cudaMemcpyDeviceToHost, st)))
+            return cuda_fail(h, ce, "copy norms");
+        if ((ce = cudaStreamSynchronize(st))) return cuda_fail(h, ce, "sync");
+        if (prm->eps > 0 && std::sqrt(norms[0]) <= prm->eps * std::sqrt(norms[1])) break;
+    }
+    *iterations = std::min(it, prm->max_iter);
+    int flag = 0;
+    if ((ce = cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost))) return cuda_fail(h, ce, "copy flag");
+    if (flag) {
+        cudaMemset(h->d_err, 0, sizeof(int));
+        return fail(h, SWEEP_E_SIGMA, (flag & 16) ? "trt_step: temperature elimination failed (non-positive or no root)"
+                                                  : "trt_step: device error flag set in the sweep");
+    }
+    return SWEEP_OK;
+}
+
 extern "C" int sweep_stats(const sweep_handle* h, long long out[4]) {
     if (!h || !out) return SWEEP_E_ARG;
     out[0] = h->launches;
@@ -775,6 +832,10 @@ extern "C" void sweep_destroy(sweep_handle* h) {
     for (auto& e : h->ev) cudaEventDestroy(e);
     cudaFree(h->d_dirs);
     cudaFree(h->d_streams);
+    cudaFree(h->d_trt_q);
+    cudaFree(h->d_trt_nu);
+    cudaFree(h->d_trt_part);
+    cudaFree(h->d_trt_norm);
     cudaFree(h->d_progress);
     cudaFree(h->d_ytr);
     cudaFree(h->d_slabs);

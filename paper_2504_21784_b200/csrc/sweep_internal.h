@@ -97,6 +97,13 @@ int sweep2d_cols_per_chunk(int p, int k, int opt);
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
 
+// unaccelerated TRT iteration (k_trt.cu)
+int trt_blocks();
+int launch_trt_emission(const double* T, const double* sigma, const double* Iprev, const double* nu, int G, int n,
+                        size_t nodes, double inv_dt, double* q, void* stream);
+int launch_trt_update(const double* Tk, double* T, const double* sphi, const double* sigma, const double* nu, int G,
+                      int n, size_t nodes, double cv_dt, double* partial, double* norms, int* err, void* stream);
+
 // per translation unit (k2d_*.cu): kernel pointer for (log2lg, k, opt), or nullptr;
 // and the upload of that unit's copy of the modal constants
 const void* pick2d_p1(int log2lg, int k);

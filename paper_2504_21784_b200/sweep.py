@@ -23,7 +23,7 @@ HALF_RANGE = 16     # also return the half-range moments F+, P+ of the consisten
 _NAMES = {1: "E_ARG", 2: "E_QUAD", 3: "E_SIGMA", 4: "E_CUDA", 5: "E_NCCL", 6: "E_INTERNAL"}
 
 # every symbol include/sweep.h declares
-EXPORTS = ("sweep_setup", "sweep_layout", "sweep_run", "closures_get", "sweep_run_host",
+EXPORTS = ("sweep_setup", "sweep_layout", "sweep_run", "closures_get", "sweep_run_host", "trt_step",
            "sweep_stats", "sweep_timing", "sweep_kernel_times", "sweep_fp64_probe",
            "sweep_nccl_unique_id", "sweep_destroy", "sweep_last_error")
 
@@ -42,6 +42,11 @@ class sweep_desc(ctypes.Structure):
                 ("group_offset", ctypes.c_int), ("n_group_total", ctypes.c_int), ("device", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("flags", ctypes.c_uint)]
+
+
+class trt_params(ctypes.Structure):
+    _fields_ = [("nu", ctypes.POINTER(ctypes.c_double)), ("cv", ctypes.c_double), ("dt", ctypes.c_double),
+                ("eps", ctypes.c_double), ("max_iter", ctypes.c_int)]
 
 
 _lib = None
@@ -66,6 +71,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.closures_get.restype = i
         lib.sweep_run_host.argtypes = [vp, dp, ctypes.c_double, dp, dp, dp, sz, vp]
         lib.sweep_run_host.restype = i
+        lib.trt_step.argtypes = [vp, dp, dp, dp, dp, ctypes.POINTER(trt_params), dp, ctypes.POINTER(i), vp]
+        lib.trt_step.restype = i
         lib.sweep_stats.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
         lib.sweep_stats.restype = i
         lib.sweep_timing.argtypes = [vp, i]
@@ -181,6 +188,24 @@ class Sweep:
                                              inflow.ctypes.data, out.ctypes.data, self.out_size,
                                              self._stream_ptr(stream)))
         return out
+
+    def trt_step(self, sigma, inflow, Tk, Iprev, nu, cv: float, dt: float, eps: float = 1e-4, max_iter: int = 50,
+                 T=None, stream=None):
+        """One unaccelerated backward-Euler TRT step (include/sweep.h trt_step): CUDA float64
+        tensors sigma [N_el][G], inflow [N_bnode][G], Tk [N_el][n], Iprev [N_el][n][G];
+        nu: host group bounds [G+1].  Returns (T tensor [N_el][n], outer iterations)."""
+        import torch
+        for t in (sigma, inflow, Tk, Iprev):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise ValueError("inputs must be contiguous float64 CUDA tensors")
+        if T is None:
+            T = torch.empty_like(Tk)
+        nu_a = np.ascontiguousarray(nu, dtype=np.float64)
+        prm = trt_params(_dptr(nu_a), float(cv), float(dt), float(eps), int(max_iter))
+        it = ctypes.c_int()
+        self._check(self._lib.trt_step(self._h, sigma.data_ptr(), inflow.data_ptr(), Tk.data_ptr(), Iprev.data_ptr(),
+                                       ctypes.byref(prm), T.data_ptr(), ctypes.byref(it), self._stream_ptr(stream)))
+        return T, it.value
 
     def stats(self) -> dict:
         a = (ctypes.c_longlong * 4)()
