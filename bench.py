@@ -205,11 +205,15 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--opts", default="", help="comma list of NEXT-row options: sigma (sigma-weighted moments), "
                                                  "fixup (zero-and-scale negative flux fixup), halfrange "
-                                                 "(half-range moments of the consistent method)")
+                                                 "(half-range moments of the consistent method), trt (one "
+                                                 "outer iteration of the unaccelerated TRT step per step: "
+                                                 "emission + sweep + temperature elimination)")
     args = ap.parse_args()
     opts = {o for o in args.opts.split(",") if o}
-    if opts - {"sigma", "fixup", "halfrange"}:
-        ap.error(f"unknown --opts {opts - {'sigma', 'fixup', 'halfrange'}}")
+    if opts - {"sigma", "fixup", "halfrange", "trt"}:
+        ap.error(f"unknown --opts {opts - {'sigma', 'fixup', 'halfrange', 'trt'}}")
+    if "trt" in opts:
+        opts.add("sigma")   # the temperature elimination consumes sum_g sigma_g phi_g
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
 
@@ -254,10 +258,23 @@ def main():
     if in_bytes < 2 * l2_bytes:
         flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
 
+    if "trt" in opts:
+        # NEXT-4: T^k per element of the config's recipe range, I^k = B_g(T^k) (input generation)
+        from synth.planck import group_bounds, planck_groups
+        nu = group_bounds(prob.G)[g0:g1 + 1]
+        Tk_np = np.repeat(np.random.default_rng(2504).uniform(0.05, 1.0, size=(prob.n_el, 1)), prob.n, axis=1)
+        Tk = torch.from_numpy(Tk_np).to(dev)
+        Ip = torch.from_numpy(planck_groups(Tk_np, nu).reshape(prob.n_el, prob.n, -1)).to(dev)
+        Tout = torch.empty_like(Tk)
+        trt_dt = 1.0 / prob.inv_c_dt
+
     def step():
         if flush.numel():
             flush.zero_()
-        sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+        if "trt" in opts:
+            sw.trt_step(sig, fl, Tk, Ip, nu, cv=1.0, dt=trt_dt, eps=0.0, max_iter=1, T=Tout)
+        else:
+            sw.sweep_run(sig, prob.inv_c_dt, q, fl)
 
     for _ in range(args.warmup):
         step()
@@ -290,11 +307,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, sweep_ms = float(t[0]), float(t[1])
     sw.closures_get(out)
-    launches_per_step = sw.stats()["launches"]
+    launches_per_step = sw.stats()["launches"] + (3 if "trt" in opts else 0)  # + emission, update, norm
 
     # ---- end to end through the host API (pinned buffers), same metric
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and "trt" not in opts:
         hs = torch.from_numpy(shard.sigma).pin_memory()
         hq = torch.from_numpy(shard.q).pin_memory()
         hf = torch.from_numpy(shard.inflow).pin_memory()

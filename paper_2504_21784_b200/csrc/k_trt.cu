@@ -12,6 +12,7 @@
 
 namespace sweepk {
 
+
 constexpr double K15_PI4 = 0.15398973382026503;  // 15 / pi^4
 
 // int_0^x t^3/(e^t-1) dt * 15/pi^4 and its derivative (15/pi^4) x^3/(e^x-1)
@@ -46,70 +47,110 @@ __device__ __forceinline__ void planck_P(double x, double& P, double& dP) {
         const double even = fma(s, x2, 0.0);
         P = K15_PI4 * x3 * (c[0] - x * 0.125 + even);
     } else {
-        // 1 - (15/pi^4) sum_n e^{-n x} (x^3/n + 3x^2/n^2 + 6x/n^3 + 6/n^4)
+        // 1 - (15/pi^4) sum_n e^{-n x} (x^3/n + 3x^2/n^2 + 6x/n^3 + 6/n^4); terms until
+        // e^{-n x} < e^{-38} (x >= 1.5: at most 27), 1/n from an unrolled table
         double tail = 0.0;
         const double e1 = exp(-x);
         double en = 1.0;
         const int nmax = (int)(38.0 / x) + 2;
-        for (int n = 1; n <= nmax; ++n) {
+        const double x6 = 6.0 * x, x23 = 3.0 * x2;
+#pragma unroll
+        for (int n = 1; n <= 27; ++n) {
+            if (n > nmax) break;
+            const double rn = 1.0 / (double)n;  // folded to a constant (unrolled)
             en *= e1;
-            const double rn = 1.0 / n;
-            tail += en * rn * (x3 + rn * (3.0 * x2 + rn * (6.0 * x + 6.0 * rn)));
+            tail = fma(en * rn, fma(rn, fma(rn, fma(6.0, rn, x6), x23), x3), tail);
         }
         P = 1.0 - K15_PI4 * tail;
     }
 }
 
-// sum_g sig_g B_g(T) and its T-derivative, nu[0..G]
-__device__ __forceinline__ void emission_sum(double T, int G, const double* __restrict__ sig,
-                                             const double* __restrict__ nu, double& E, double& dE) {
-    const double T3 = T * T * T, T4 = T3 * T, iT = 1.0 / T;
-    double Pl, dPl;
-    double xl = nu[0] * iT;
-    planck_P(xl, Pl, dPl);
-    E = 0.0;
-    dE = 0.0;
-    for (int g = 0; g < G; ++g) {
-        const double xr = nu[g + 1] * iT;
-        double Pr, dPr;
-        planck_P(xr, Pr, dPr);
-        const double s = sig[g];
-        E = fma(s, T4 * (Pr - Pl), E);
-        // dB/dT = 4 T^3 (Pr - Pl) - T^3 (xr P'(xr) - xl P'(xl))
-        dE = fma(s, T3 * (4.0 * (Pr - Pl) - (xr * dPr - xl * dPl)), dE);
-        Pl = Pr;
-        dPl = dPr;
-        xl = xr;
-    }
-}
-
-// q[v][g] = sigma[e][g] B_g(T[v]) + Iprev[v][g] * inv_dt   (v = e*n + k)
+// q[v][g] = sigma[e][g] B_g(T[v]) + Iprev[v][g] * inv_dt   (v = e*n + k).  One thread per
+// (node, group); each evaluates P at its upper bound only and takes the lower bound's value
+// from the neighbouring lane (the groups of a node are consecutive lanes); the first group
+// of a warp segment evaluates its lower bound itself.
 __global__ void trt_emission_kernel(const double* __restrict__ T, const double* __restrict__ sigma,
                                     const double* __restrict__ Iprev, const double* __restrict__ nu, int G, int n,
                                     size_t nodes, double inv_dt, double* __restrict__ q) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nodes * G; i += (size_t)gridDim.x * blockDim.x) {
-        const size_t v = i / G;
-        const int g = (int)(i - v * G);
-        const size_t e = v / n;
+    const size_t total = nodes * G;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (size_t i0 = (size_t)blockIdx.x * blockDim.x; i0 < total; i0 += stride) {
+        const size_t i = i0 + threadIdx.x;
+        const bool on = i < total;
+        const size_t ii = on ? i : total - 1;
+        const size_t v = ii / G;
+        const int g = (int)(ii - v * G);
         const double t = T[v];
-        double Pl, Pr, d;
-        planck_P(nu[g] / t, Pl, d);
-        planck_P(nu[g + 1] / t, Pr, d);
-        const double t2 = t * t;
-        q[i] = fma(sigma[e * G + g], t2 * t2 * (Pr - Pl), Iprev[i] * inv_dt);
+        const double it = 1.0 / t;
+        double Pr, d;
+        planck_P(nu[g + 1] * it, Pr, d);
+        double Pl = __shfl_up_sync(0xffffffffu, Pr, 1);
+        const double lo_from_left = __shfl_up_sync(0xffffffffu, (double)v, 1);
+        if (g == 0 || lane == 0 || lo_from_left != (double)v) planck_P(nu[g] * it, Pl, d);
+        if (on) {
+            const size_t e = v / n;
+            const double t2 = t * t;
+            q[ii] = fma(sigma[e * G + g], t2 * t2 * (Pr - Pl), Iprev[ii] * inv_dt);
+        }
     }
 }
 
-// per node: solve cv_dt (T - Tk) + E(T) = sphi by bracketed Newton from the current
-// iterate T; writes the new T and per-block partial sums of (dT^2, T^2) for the
-// convergence test (summed in a fixed order afterwards: deterministic)
+// sum_g sig_g B_g(T) and its T-derivative over the groups, one warp per node: lane l
+// evaluates P at the bounds b = l, l + 32, ... and owns group g = b - 1 (its lower bound
+// comes from the neighbouring lane, or from lane 31 of the previous round); fixed-order
+// butterfly sums, so every lane ends with the same E, dE
+__device__ __forceinline__ void emission_sum_warp(double T, int G, const double* __restrict__ sig,
+                                                  const double* __restrict__ nu, int lane, double& E, double& dE) {
+    const double T3 = T * T * T, T4 = T3 * T, iT = 1.0 / T;
+    double e = 0.0, de = 0.0;
+    double carry_P = 0.0, carry_x = 0.0, carry_dP = 0.0;  // bound 32k - 1 (lane 31 of the previous round)
+    for (int b0 = 0; b0 <= G; b0 += 32) {
+        const int bnd = b0 + lane;
+        double P = 0.0, dP = 0.0, x = 0.0;
+        if (bnd <= G) {
+            x = nu[bnd] * iT;
+            planck_P(x, P, dP);
+        }
+        double Pl = __shfl_up_sync(0xffffffffu, P, 1), dPl = __shfl_up_sync(0xffffffffu, dP, 1),
+               xl = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) {
+            Pl = carry_P;
+            dPl = carry_dP;
+            xl = carry_x;
+        }
+        if (bnd >= 1 && bnd <= G) {
+            const double sg = sig[bnd - 1];
+            e = fma(sg, T4 * (P - Pl), e);
+            de = fma(sg, T3 * (4.0 * (P - Pl) - (x * dP - xl * dPl)), de);
+        }
+        carry_P = __shfl_sync(0xffffffffu, P, 31);
+        carry_dP = __shfl_sync(0xffffffffu, dP, 31);
+        carry_x = __shfl_sync(0xffffffffu, x, 31);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        de += __shfl_xor_sync(0xffffffffu, de, o);
+    }
+    E = e;
+    dE = de;
+}
+
+// per node (one warp): solve cv_dt (T - Tk) + E(T) = sphi by a bracketed Newton
+// iteration from the current iterate T; writes the new T and per-block partial sums of
+// (dT^2, T^2) for the convergence test (summed in a fixed order afterwards).  One warp
+// per node: nodes converge after different numbers of steps, and a thread per node
+// made every warp wait for its slowest node.
 __global__ void __launch_bounds__(256) trt_update_kernel(const double* __restrict__ Tk, double* __restrict__ T,
                                                          const double* __restrict__ sphi, const double* __restrict__ sigma,
                                                          const double* __restrict__ nu, int G, int n, size_t nodes,
                                                          double cv_dt, double* __restrict__ partial, int* err) {
-    __shared__ double red[2][256];
+    __shared__ double red[2][8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     double dsq = 0.0, tsq = 0.0;
-    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += (size_t)gridDim.x * blockDim.x) {
+    const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
+    for (size_t v = (size_t)blockIdx.x * (blockDim.x >> 5) + wib; v < nodes; v += warps) {
         const double* sg = sigma + (v / n) * G;
         const double tk = Tk[v], s = sphi[v], told = T[v];
         double t = told > 0.0 ? told : (tk > 0.0 ? tk : 1.0);
@@ -117,7 +158,7 @@ __global__ void __launch_bounds__(256) trt_update_kernel(const double* __restric
         bool ok = false;
         for (int it = 0; it < 100; ++it) {
             double E, dE;
-            emission_sum(t, G, sg, nu, E, dE);
+            emission_sum_warp(t, G, sg, nu, lane, E, dE);
             const double f = fma(cv_dt, t - tk, E - s);
             if (f == 0.0) {
                 ok = true;
@@ -125,33 +166,46 @@ __global__ void __launch_bounds__(256) trt_update_kernel(const double* __restric
             }
             if (f < 0.0) lo = t;
             else hi = t;
-            double tn = t - f / (cv_dt + dE);
+            // Newton step in v = T^m, m = t E'/E the local power-law exponent of the
+            // emission: exact in one step for a single power law, so cooling nodes whose
+            // root lies far below T (emission ~ T^4 >> the absorbed sphi) do not creep down
+            // by the factor 3/4 per step plain Newton would take; to first order it is the
+            // plain Newton step T - f/f'
+            const double fp = cv_dt + dE;
+            const double m = (E > 0.0) ? fmax(1.0, t * dE / E) : 1.0;
+            const double r = 1.0 - m * f / (t * fp);
+            double tn = (r > 0.0) ? t * exp(log(r) / m) : 0.0;  // 0: rejected by the bracket below
             if (!(tn > lo) || (hi > 0.0 && !(tn < hi))) tn = (hi > 0.0) ? 0.5 * (lo + hi) : 2.0 * t;
-            const bool done = fabs(tn - t) <= 1e-15 * tn;
+            // converged: a step below 1e-13 relative (the iterate after it is exact to rounding:
+            // quadratic convergence; smaller thresholds sit below the rounding noise of f), or
+            // the sign bracket that narrow
+            const bool done = fabs(tn - t) <= 1e-13 * tn || (hi > 0.0 && hi - lo <= 1e-15 * hi);
             t = tn;
             if (done) {
                 ok = true;
                 break;
             }
         }
-        if (!ok || !(t > 0.0) || !(t < 1e300)) atomicOr(err, 16);
-        T[v] = t;
-        dsq = fma(t - told, t - told, dsq);
-        tsq = fma(t, t, tsq);
-    }
-    red[0][threadIdx.x] = dsq;
-    red[1][threadIdx.x] = tsq;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + w];
-            red[1][threadIdx.x] += red[1][threadIdx.x + w];
+        if (lane == 0) {
+            if (!ok || !(t > 0.0) || !(t < 1e300)) atomicOr(err, 16);
+            T[v] = t;
+            dsq = fma(t - told, t - told, dsq);
+            tsq = fma(t, t, tsq);
         }
-        __syncthreads();
     }
+    if (lane == 0) {
+        red[0][wib] = dsq;
+        red[1][wib] = tsq;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        partial[2 * blockIdx.x] = red[0][0];
-        partial[2 * blockIdx.x + 1] = red[1][0];
+        double a = 0.0, c = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += red[0][w];
+            c += red[1][w];
+        }
+        partial[2 * blockIdx.x] = a;
+        partial[2 * blockIdx.x + 1] = c;
     }
 }
 
