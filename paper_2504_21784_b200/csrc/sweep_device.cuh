@@ -349,12 +349,20 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 // Strip / chunk geometry as a function of (P, K): T element rows per strip,
 // C columns per chunk (one pipeline step).  K >= 4 lanes carry many groups, so
 // fewer rows keep the x-traces in registers.
-__host__ __device__ constexpr int rows_per_strip(int P, int K) { return K >= 4 ? 2 : (K == 2 ? 4 : (P == 2 ? 4 : 8)); }
+#ifndef SWEEP_ROWS_P1K1
+#define SWEEP_ROWS_P1K1 4  // C3: 0.53 -> 0.34 ms vs 8 rows; C4 unchanged (round-1 sweep of 2-16 rows x 2-8 columns)
+#endif
+#ifndef SWEEP_COLS_K1
+#define SWEEP_COLS_K1 4
+#endif
+__host__ __device__ constexpr int rows_per_strip(int P, int K) {
+    return K >= 4 ? 2 : (K == 2 ? 4 : (P == 2 ? 4 : SWEEP_ROWS_P1K1));
+}
 #ifndef SWEEP_COLS_K4
 #define SWEEP_COLS_K4 8
 #endif
 __host__ __device__ constexpr int cols_per_chunk(int P, int K, int OPT = 0) {
-    return K >= 4 ? ((OPT & OPT_SIGMA) ? 4 : SWEEP_COLS_K4) : 4;  // sigma moments: a second S buffer, half the chunk
+    return K >= 4 ? ((OPT & OPT_SIGMA) ? 4 : SWEEP_COLS_K4) : SWEEP_COLS_K1;  // sigma moments: a second S buffer, half the chunk
 }
 // (K = 2: T = 4 rows, C = 4 columns -> 16 elements per chunk, like K = 4)
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
