@@ -426,10 +426,18 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     const int gbw = std::min(32, 1 << ilog2_ceil(h->G));
     // 2-D p=2 with many groups: 4 groups per lane over 16 lanes (one CTA holds a
     // whole quadrant's directions); otherwise 1 group per lane over up to 32 lanes
+    // (measured per-rank workloads of the group-sharded C5: 64 groups 4x16,
+    // 32 groups 2x16, 16 groups 2x8; fewer: one group per lane.  With options only the
+    // 4x16 and one-group layouts are instantiated.)
+    const bool opt_layouts_only = h->opt != 0;
     if (D.dim == 2 && D.p == 2 && h->G >= 64) {
         h->kpl = 4;
         h->gb = 16;
         h->log2gb = 4;
+    } else if (D.dim == 2 && D.p == 2 && h->G >= 16 && !opt_layouts_only) {
+        h->kpl = 2;
+        h->gb = (h->G >= 32) ? 16 : 8;
+        h->log2gb = (h->G >= 32) ? 4 : 3;
     } else {
         h->kpl = 1;
         h->gb = gbw;
