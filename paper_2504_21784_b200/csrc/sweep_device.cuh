@@ -738,7 +738,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
             const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)(K * NT) * NL;
             double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)(K * NT) * NL;
             const bool write_y = J + 1 < prm.n_strips;
-#pragma unroll 1
+#ifndef SWEEP_COL_UNROLL
+#define SWEEP_COL_UNROLL 1
+#endif
+            constexpr int kColUnroll = SWEEP_COL_UNROLL;
+#pragma unroll kColUnroll
             for (int col = 0; col < C; ++col) {
                 const int ip = i0 + col;
                 double ty[K][NT];
