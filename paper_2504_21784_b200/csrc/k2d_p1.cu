@@ -1,4 +1,5 @@
 // k2d_p1.cu — instantiates the 2-D p = 1 sweep kernels without options (compiled in parallel with the other k_*.cu units).
+#define SWEEP_TRACE_OWNER sweep_debug_trace_p1
 #include "sweep_device.cuh"
 
 namespace sweepk {

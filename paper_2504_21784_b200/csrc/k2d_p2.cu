@@ -1,5 +1,5 @@
 // k2d_p2.cu — instantiates the 2-D p = 2 sweep kernels without options (compiled in parallel with the other k_*.cu units).
-#define SWEEP_TRACE_OWNER
+#define SWEEP_TRACE_OWNER sweep_debug_trace
 #include "sweep_device.cuh"
 
 namespace sweepk {

@@ -49,7 +49,8 @@ __device__ __forceinline__ long long gtimer() {
     return t;
 }
 #ifdef SWEEP_TRACE_OWNER
-extern "C" int sweep_debug_trace(long long* host, int n) {
+// SWEEP_TRACE_OWNER names this unit's accessor (sweep_debug_trace: p = 2, _p1: p = 1)
+extern "C" int SWEEP_TRACE_OWNER(long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 8 * (size_t)n);
 }
 #endif

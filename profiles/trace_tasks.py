@@ -16,8 +16,7 @@ import torch  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 so = "/tmp/libsweep_trace.so"
-subprocess.check_call([B.nvcc(), *B.NVCC_FLAGS, "-DSWEEP_TRACE", "-I", os.path.join(ROOT, "include"), "-o", so,
-                       *B.SOURCES])
+B.build(extra=["-DSWEEP_TRACE"], out=so)
 S._lib = None
 lib = S.load_library(so)
 prob = synth.config(cfg)
@@ -33,8 +32,9 @@ sw.sweep_run(sig, prob.inv_c_dt, q, fl)
 kt = sw.kernel_times(1)
 ntask = 4096
 buf = (ctypes.c_longlong * (8 * ntask))()
-lib.sweep_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-lib.sweep_debug_trace(buf, ntask)
+acc = lib.sweep_debug_trace if prob.p == 2 else lib.sweep_debug_trace_p1  # per-unit trace buffer
+acc.argtypes = [ctypes.c_void_p, ctypes.c_int]
+acc(buf, ntask)
 a = np.array(buf).reshape(-1, 8)
 a = a[a[:, 1] > 0]
 t0 = a[:, 0].min()
