@@ -191,17 +191,16 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     const double e11 = st + L.A11;
     const double e11s = e11 * e11;
     const double m11 = e11s + L.I11s, m12 = e11s + L.I12s;
-    // one reciprocal for the five real denominators
-    const double p1 = d00 * m01, p2 = p1 * m10, p3 = p2 * m11, p4 = p3 * m12;
-    double inv = rcp64_fast(p4);
-    const double i12 = inv * p3;
-    inv *= m12;
-    const double i11 = inv * p2;
-    inv *= m11;
-    const double i10 = inv * p1;
-    inv *= m10;
-    const double i01 = inv * d00;
-    const double i00 = inv * m01;
+    // one reciprocal for the five real denominators (Montgomery's trick), tree form:
+    // 12 multiplications at dependency depth 3 + 3 (the linear chain: 4 + 4; C5 -0.5 %)
+    const double pa = d00 * m01, pb = m10 * m11;
+    const double pab = pa * pb, p4 = pab * m12;
+    const double inv = rcp64_fast(p4);
+    const double i12 = inv * pab;
+    const double iab = inv * m12;
+    const double ia = iab * pb, ib = iab * pa;
+    const double i00 = ia * m01, i01 = ia * d00;
+    const double i10 = ib * m11, i11 = ib * m10;
 
     u[0] = r00 * i00;
     u[1] = (r01r * e01 + r01i * L.I01) * i01;
