@@ -160,7 +160,9 @@ __global__ void __launch_bounds__(256) trt_update_kernel(const double* __restric
             double E, dE;
             emission_sum_warp(t, G, sg, nu, lane, E, dE);
             const double f = fma(cv_dt, t - tk, E - s);
-            if (f == 0.0) {
+            // converged to the rounding noise of f (a few ulps of its largest term): a Newton
+            // step from here would only chase that noise (and fall back to bisection)
+            if (fabs(f) <= 4e-16 * (cv_dt * (t + tk) + E + fabs(s))) {
                 ok = true;
                 break;
             }

@@ -84,6 +84,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -355,8 +360,11 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 #ifndef SWEEP_COLS_K1
 #define SWEEP_COLS_K1 4
 #endif
+#ifndef SWEEP_ROWS_K4
+#define SWEEP_ROWS_K4 2
+#endif
 __host__ __device__ constexpr int rows_per_strip(int P, int K) {
-    return K >= 4 ? 2 : (K == 2 ? 4 : (P == 2 ? 4 : SWEEP_ROWS_P1K1));
+    return K >= 4 ? SWEEP_ROWS_K4 : (K == 2 ? 4 : (P == 2 ? 4 : SWEEP_ROWS_P1K1));
 }
 #ifndef SWEEP_COLS_K4
 #define SWEEP_COLS_K4 8
@@ -711,13 +719,19 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
 #ifdef SWEEP_TRACE
                 const long long w0 = gtimer();
 #endif
-                while (ld_acquire(f) < c + 1) {
-                    __nanosleep(32);
+                // poll with relaxed loads (an acquire load invalidates the SM's L1 on every
+                // iteration), then one acquire load to order the trace reads after the flag
+#ifndef SWEEP_POLL_NS
+#define SWEEP_POLL_NS 0
+#endif
+                while (ld_relaxed_gpu(f) < c + 1) {
+                    if (SWEEP_POLL_NS > 0) __nanosleep(SWEEP_POLL_NS);
                     if (clock64() - t_start > (1LL << 34)) {
                         atomicOr(prm.err, 4);
                         break;
                     }
                 }
+                (void)ld_acquire(f);
 #ifdef SWEEP_TRACE
                 t_waited += gtimer() - w0;
 #endif
