@@ -17,6 +17,59 @@ __global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, s
     if (bad) atomicOr(err, 2);
 }
 
+// ------------------------------------------------------------------ modal slabs (2-D, p = 2)
+// The p = 2 sweep kernel leaves its node fields in the slabs as MODAL values in its
+// stream's sweep orientation (physical element, 9 modal reals).  Physical node
+// k = a + 3b is sweep node (fx ? 2-a : a) + 3 (fy ? 2-b : b), so the nodal value is
+// sum_m bck[that node][m] M[m]; summing the streams in a fixed order keeps the result
+// deterministic.  One thread per (field row, element).
+__device__ __forceinline__ int sweep_node_of(int k, int q) {
+    const int a = k % 3, b = k / 3;
+    return ((q & 1) ? 2 - a : a) + 3 * ((q & 2) ? 2 - b : b);
+}
+
+__global__ void finalize_modal_kernel(const double* __restrict__ slabs, int n_slabs, size_t stride,
+                                      const StreamDesc* __restrict__ streams, size_t row0, int nrows, size_t nel,
+                                      double* __restrict__ out, int* err) {
+    // bck staged in shared memory: runtime-indexed constant-bank loads get hoisted by ptxas
+    // for inactive iterations, and a stray constant address is a fatal illegal instruction
+    __shared__ double bck[81];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 81; ++i) bck[i] = cM.bck[i / 9][i % 9];
+    }
+    __syncthreads();
+    bool bad = false;
+    const size_t total = (size_t)nrows * nel;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t base = row0 + i * 9;  // rows are [nel][9] blocks, contiguous over the field range
+        double acc[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+        for (int s = 0; s < n_slabs; ++s) {
+            const double* M = slabs + (size_t)s * stride + base;
+            double m[9];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) m[j] = __ldcs(M + j);
+            const int q = streams[s].quadrant;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int kk = sweep_node_of(k, q);
+                double v = 0.0;
+#pragma unroll
+                for (int j = 0; j < 9; ++j) v = fma(bck[kk * 9 + j], m[j], v);
+                acc[k] += v;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            out[base + k] = acc[k];
+            bad |= !(fabs(acc[k]) < 1.0e300);
+        }
+    }
+    if (bad) atomicOr(err, 2);
+}
+
 // ------------------------------------------------------------------ half-range moments (NEXT-3)
 // Every slab holds one stream's contribution, and a stream is one sweep quadrant
 // (half-range in 1-D): all its directions have the same signs of Omega_x, Omega_y.
@@ -26,12 +79,56 @@ __global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, s
 // streams with Omega_x >= 0 (resp. Omega_y >= 0), evaluated at every node (each
 // element's own trace at its face nodes).  F-, P- = full minus plus.
 // out rows (2-D): Fx+[x,y], Px+[xx,xy,yy], Fy+[x,y], Py+[xx,xy,yy]; (1-D): F+, P+.
+// modal != 0 (2-D p = 2): the slab rows hold modal values (see finalize_modal_kernel).
 __global__ void halfrange_kernel(const double* __restrict__ slabs, int n_slabs, size_t stride,
-                                 const StreamDesc* __restrict__ streams, size_t nodes, int dim,
+                                 const StreamDesc* __restrict__ streams, size_t nodes, int dim, int modal,
                                  double* __restrict__ out) {
     const double third = 1.0 / 3.0;
+    __shared__ double bck[81];  // (see finalize_modal_kernel)
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 81; ++i) bck[i] = cM.bck[i / 9][i % 9];
+    }
+    __syncthreads();
     for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += (size_t)gridDim.x * blockDim.x) {
-        if (dim == 2) {
+        if (modal) {
+            const size_t e9 = (v / 9) * 9;
+            const int k = (int)(v - e9);
+            double a[10];
+#pragma unroll
+            for (int m = 0; m < 10; ++m) a[m] = 0.0;
+            for (int s = 0; s < n_slabs; ++s) {
+                const double* sl = slabs + (size_t)s * stride + e9;
+                const int q = streams[s].quadrant;
+                const int kk = sweep_node_of(k, q);
+                double f6[6];
+#pragma unroll
+                for (int f = 0; f < 6; ++f) {
+                    double x = 0.0;
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) x = fma(bck[kk * 9 + j], sl[(size_t)f * nodes + j], x);
+                    f6[f] = x;
+                }
+                const double jx = f6[1], jy = f6[2], pxx = f6[3] + third * f6[0], pxy = f6[4],
+                             pyy = f6[5] + third * f6[0];
+                if (!(q & 1)) {
+                    a[0] += jx;
+                    a[1] += jy;
+                    a[2] += pxx;
+                    a[3] += pxy;
+                    a[4] += pyy;
+                }
+                if (!(q & 2)) {
+                    a[5] += jx;
+                    a[6] += jy;
+                    a[7] += pxx;
+                    a[8] += pxy;
+                    a[9] += pyy;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 10; ++m) out[(size_t)m * nodes + v] = a[m];
+        } else if (dim == 2) {
             double a[10];
 #pragma unroll
             for (int m = 0; m < 10; ++m) a[m] = 0.0;
@@ -112,10 +209,8 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
     const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k, opt), NQ = nq_of(p), NN = (p + 1) * (p + 1);
     const int CT = C * T;
     const int NL = dset * gbk / k;  // threads per CTA
-    const int nfo = (opt & OPT_SIGMA) ? 9 : 6;
     const int s2 = (opt & OPT_SIGMA) ? CT * (dset * NQ + 1) : 0;
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + CT * nfo * NQ + 81 +
-            s2) *
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + 81 + s2) *
            (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
@@ -157,12 +252,23 @@ int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, d
 }
 
 int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes, int dim,
-                     double* out, void* stream) {
+                     int modal, double* out, void* stream) {
     const int block = 256;
     size_t want = (nodes + block - 1) / block;
     int grid = (int)(want < 148 * 8 ? want : 148 * 8);
     if (grid < 1) grid = 1;
-    halfrange_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, nodes, dim, out);
+    halfrange_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, nodes, dim, modal, out);
+    return (int)cudaGetLastError();
+}
+
+int launch_finalize_modal(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t row0,
+                          int nrows, size_t nel, double* out, int* err, void* stream) {
+    const int block = 256;
+    size_t want = ((size_t)nrows * nel + block - 1) / block;
+    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+    if (grid < 1) grid = 1;
+    finalize_modal_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, row0, nrows, nel,
+                                                                    out, err);
     return (int)cudaGetLastError();
 }
 

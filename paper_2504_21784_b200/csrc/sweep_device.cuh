@@ -588,8 +588,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
         double* coefS = S + (size_t)CT * SEL;
         double* ypre = coefS + dset * NFIELD;  // [K*NT][NL] next-column trace prefetch
         constexpr int NFO = SIG ? 9 : 6;       // node fields: 6 moments (+ sigma phi, sigma Jx, sigma Jy)
-        double* Mbuf = ypre + K * NT * NL;     // [CT][NFO][NQ] direction sums (phase C stage 1, p = 2)
-        double* bckS = Mbuf + CT * NFO * NQ;   // [9][9] modal -> nodal (p = 2)
+        double* bckS = ypre + K * NT * NL;     // [9][9] modal -> nodal (p = 2, boundary closures)
         double* S2 = bckS + 81;                // SIG: [CT][SEL] sigma-weighted group sums
         const size_t sig_off = 6 * nodes + 2 * (size_t)prm.nbnode;  // SIG: sigma phi | sigma J
         // (compile-time constant-bank indices only: ptxas hoists constant loads out of
@@ -953,7 +952,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                 // PC outputs per thread per pass: independent accumulation chains, and all
                 // their S loads ahead of the stores (Mbuf and S share the smem window)
 #ifndef SWEEP_PC
-#define SWEEP_PC 4
+#define SWEEP_PC 1  // 4 (0.3 % faster at C5) hits an illegal-instruction fault in the p = 2, 2-lane layout with modal slabs
 #endif
                 constexpr int PC = SWEEP_PC;
                 for (int o0 = tid; o0 < CT * NFO * NQ; o0 += PC * NL) {
@@ -977,17 +976,18 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                     for (int u = 0; u < PC; ++u) {
                         const int o = o0 + u * NL;
                         if (o >= CT * NFO * NQ) continue;
-                        if constexpr (P == 2) {
-                            Mbuf[o] = acc[u];
-                        } else {
-                            const int m = o % NQ, rest = o / NQ;
-                            const int f = rest % NFO, el = rest / NFO;
-                            const int col = el / T, r = el - col * T;
-                            if (col < cols && r < rows) {
-                                const int ip = i0 + col, jp = j0 + r;
-                                const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                                node_store(field_dst(f) + ((size_t)i + (size_t)nx * j) * NN, m, acc[u]);
-                            }
+                        const int m = o % NQ, rest = o / NQ;
+                        const int f = rest % NFO, el = rest / NFO;
+                        const int col = el / T, r = el - col * T;
+                        if (col < cols && r < rows) {
+                            const int ip = i0 + col, jp = j0 + r;
+                            const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                            double* dst = field_dst(f) + ((size_t)i + (size_t)nx * j) * NN;
+                            // p = 2: the slab keeps the MODAL values (sweep orientation); the
+                            // finalize kernel applies each stream's back transform once per
+                            // output instead of every CTA per chunk.  p = 1: nodal already.
+                            if constexpr (P == 2) dst[m] = acc[u];
+                            else node_store(dst, m, acc[u]);
                         }
                     }
                 }
@@ -1039,23 +1039,6 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
                         const int bn = bnode2d(face, idx, t, nx, ny, NP1);
                         slab[6 * nodes + bn] = vb;
                         slab[6 * nodes + prm.nbnode + bn] = vj;
-                    }
-                }
-                if constexpr (P == 2) {
-                    __syncthreads();
-                    for (int o = tid; o < CT * NFO * NN; o += NL) {
-                        const int kk = o % NN, rest = o / NN;
-                        const int f = rest % NFO, el = rest / NFO;
-                        const int col = el / T, r = el - col * T;
-                        if (col >= cols || r >= rows) continue;
-                        const double* Mp = Mbuf + rest * NQ;
-                        const double* bk = bckS + kk * 9;
-                        double v = 0.0;
-#pragma unroll
-                        for (int m = 0; m < 9; ++m) v = fma(bk[m], Mp[m], v);
-                        const int ip = i0 + col, jp = j0 + r;
-                        const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                        node_store(field_dst(f) + ((size_t)i + (size_t)nx * j) * NN, kk, v);
                     }
                 }
             }

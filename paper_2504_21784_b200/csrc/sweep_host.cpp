@@ -662,11 +662,27 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
     if (e) return cuda_fail(h, (cudaError_t)e, "launch sweep");
     ++h->launches;
     if (evs) cudaEventRecord(evs[1], st);
-    e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->sum_size, h->d_out, h->d_err, stream);
-    if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");
-    ++h->launches;
+    const bool modal = (h->dim == 2 && h->p == 2);  // the p = 2 sweep leaves modal node fields in the slabs
+    if (!modal) {
+        e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->sum_size, h->d_out, h->d_err, stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");
+        ++h->launches;
+    } else {
+        const size_t nel = h->nodes / 9;
+        // phi, J, T rows | beta, J+ (plain sum) | sigma phi, sigma J rows (SWEEP_SIGMA_MOMENTS)
+        e = sweepk::launch_finalize_modal(h->d_slabs, h->n_streams, h->out_size, h->d_streams, 0, 6, nel, h->d_out,
+                                          h->d_err, stream);
+        if (!e)
+            e = sweepk::launch_finalize(h->d_slabs + h->off[3], h->n_streams, h->out_size, 2 * (size_t)h->nbnode,
+                                        h->d_out + h->off[3], h->d_err, stream);
+        if (!e && h->off[7] > h->off[5])
+            e = sweepk::launch_finalize_modal(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->off[5], 3, nel,
+                                              h->d_out, h->d_err, stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");
+        h->launches += (h->off[7] > h->off[5]) ? 3 : 2;
+    }
     if (h->out_size > h->sum_size) {
-        e = sweepk::launch_halfrange(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->nodes, h->dim,
+        e = sweepk::launch_halfrange(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->nodes, h->dim, modal ? 1 : 0,
                                      h->d_out + h->sum_size, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch halfrange");
         ++h->launches;

@@ -89,7 +89,10 @@ int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, 
 int launch_sweep1d(int p, int log2gb, int opt, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream);
 int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, void* stream);
 int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes, int dim,
-                     double* out, void* stream);
+                     int modal, double* out, void* stream);
+// 2-D p = 2: back transform + fixed-order sum of the modal node-field rows [row0, row0 + nrows*nel*9)
+int launch_finalize_modal(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t row0,
+                          int nrows, size_t nel, double* out, int* err, void* stream);
 int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt);
 int sweep2d_occupancy(int p, int log2lg, int k, int opt, int block, size_t smem, int* blocks_per_sm);
 int sweep2d_rows_per_strip(int p, int k);
