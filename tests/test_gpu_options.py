@@ -116,3 +116,25 @@ def test_sigma_moments_keep_base_fields(pk):
     a = pk.run_problem(prob)
     b = pk.run_problem(prob, flags=pk.SIGMA_MOMENTS)
     assert np.abs(b[:a.size] - a).max() <= 1e-14 * np.abs(a).max()
+
+
+def test_options_config5_full_size_replicated(pk):
+    """C5 at full size (512^2, p = 2, 128 directions, 64 groups: the many-group layout
+    and the bench launch configuration) with every option on.  The 64 groups carry the
+    data of 4 distinct C5 groups; every output is a sum over groups of per-(d, g) terms
+    (the fixup acts per (d, g) too), so gray(GPU) = 16 x sum over the 4 oracle groups."""
+    from synth.configs import Problem, replicate_groups
+    prob = synth.config(5)
+    distinct = [0, 21, 42, 63]
+    rep = replicate_groups(prob, distinct)
+    opts = SIG | FIX | HR
+    got = pk.run_problem(rep, flags=_flags(pk, opts))
+    ref = None
+    for g in distinct:
+        sub = Problem("c5g", 2, 512, 512, 2, prob.omega, prob.w, np.ascontiguousarray(prob.sigma[:, g:g + 1]),
+                      np.ascontiguousarray(prob.q[:, :, g:g + 1]), np.ascontiguousarray(prob.inflow[:, g:g + 1]),
+                      prob.inv_c_dt)
+        r = oracle.sweep(sub, opts=opts)
+        ref = r if ref is None else ref + r
+    ref *= rep.sigma.shape[1] // len(distinct)
+    assert_parity(got, ref, 2, 512, 512, 2, sigma_moments=True, half_range=True)
