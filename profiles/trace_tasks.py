@@ -48,3 +48,8 @@ print(f"cycles (thread 0): A+wait {a[:, 4].sum() / tot_cyc:.3f}  B {a[:, 5].sum(
 print(f"last end {end.max():.1f} us; sum(dur)/ctas {dur.sum() / st['ctas']:.1f} us")
 for k in range(0, len(a), max(1, len(a) // 24)):
     print(f"  task {k:5d} sm {a[k, 3]:3d} start {start[k]:9.1f} end {end[k]:9.1f} wait {wait[k]:8.1f}")
+# per-task phase split (thread 0 cycles) of the first tasks (J = 0 strips: no waiting)
+for k in range(min(4, len(a))):
+    tot = (a[k, 1] - a[k, 0]) * 1e-9 * 1.965e9
+    print(f"  task {k}: A+wait {a[k, 4] / tot:.3f}  B {a[k, 5] / tot:.3f}  C+loop {1 - (a[k, 4] + a[k, 5]) / tot:.3f}  "
+          f"({(a[k, 1] - a[k, 0]) / 1e3:.1f} us)")
