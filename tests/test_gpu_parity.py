@@ -222,3 +222,24 @@ def test_host_api_matches_device_api(lib):
     with pk.from_problem(prob) as sw:
         b = sw.sweep_run_host(prob.sigma, prob.inv_c_dt, prob.q, prob.inflow)
     assert np.array_equal(a, b)
+
+
+def test_nccl_allreduce_plumbing_one_rank(lib, monkeypatch):
+    """The NCCL path (dlopen of the libnccl torch loaded, ncclGetUniqueId, ncclCommInitRank,
+    the in-place ncclAllReduce on the sweep's stream, ncclCommDestroy) on a 1-rank
+    communicator (SWEEP_FORCE_NCCL): the output equals the plain run bit for bit."""
+    import torch
+    prob = synth.config(4, nx=24, G=6)
+    plain = gpu_out(lib, prob)
+    monkeypatch.setenv("SWEEP_FORCE_NCCL", "1")
+    nid = lib.nccl_unique_id()
+    dev = torch.device("cuda:0")
+    with lib.from_problem(prob, nranks=1, rank=0, nccl_id=nid) as sw:
+        s, q, f = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (prob.sigma, prob.q, prob.inflow))
+        sw.timing(True)
+        for _ in range(3):
+            sw.sweep_run(s, prob.inv_c_dt, q, f)
+        got = sw.closures_get().cpu().numpy()
+        kt = sw.kernel_times(3)
+    assert np.array_equal(got, plain)
+    assert (kt[:, 2] >= 0).all()
