@@ -284,26 +284,35 @@ __device__ __forceinline__ bool fixup_nodal(double (&x)[N], const double (&W)[N]
     }
     return true;
 }
-// p = 2, modal u: nodal values (V (x) V) u, fixup, back to modal (W (x) W)
+// p = 2 modal -> nodal map (V (x) V) applied one axis at a time (58 FMA + 4 adds
+// instead of the 81 of the dense 9 x 9 map; modal_forward is the W (x) W analogue).  Modal reals
+// m = [u00, u01r, u01i, u10r, u10i, u11r, u11i, u12r, u12i] (first index x mode, second
+// y mode; u02 = conj u01, u20 = conj u10, u22 = conj u11, u21 = conj u12); nodal k = a + 3b.
+__device__ __forceinline__ void modal_to_nodal_p2(const double (&u)[9], double (&x)[9]) {
+    // y pass: y0(b) = u00 V0b + 2 Re(u01 V1b),  y1(b) = u10 V0b + u11 V1b + u12 conj(V1b)
+    const double sr = u[5] + u[7], dr = u[5] - u[7], si = u[6] + u[8], di = u[8] - u[6];
+    double y0[3], y1r[3], y1i[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        y0[b] = fma(u[0], cM.V0[b], fma(u[1], cM.V1re2[b], u[2] * cM.V1im2n[b]));
+        y1r[b] = fma(u[3], cM.V0[b], fma(sr, cM.V1re[b], di * cM.V1im[b]));
+        y1i[b] = fma(u[4], cM.V0[b], fma(si, cM.V1re[b], dr * cM.V1im[b]));
+    }
+    // x pass: x(a, b) = V0a y0(b) + 2 Re(V1a y1(b))
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            x[a + 3 * b] = fma(cM.V0[a], y0[b], fma(cM.V1re2[a], y1r[b], cM.V1im2n[a] * y1i[b]));
+}
+// p = 2, modal u: nodal values, zero-and-scale, back to modal
 __device__ __forceinline__ bool fixup_p2(double (&u)[9]) {
     double x[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-        double acc = 0.0;
-#pragma unroll
-        for (int m = 0; m < 9; ++m) acc = fma(cM.bck[k][m], u[m], acc);
-        x[k] = acc;
-    }
+    modal_to_nodal_p2(u, x);
     constexpr double w0 = 1.0 / 6.0, w1 = 2.0 / 3.0;
     const double W[9] = {w0 * w0, w1 * w0, w0 * w0, w0 * w1, w1 * w1, w0 * w1, w0 * w0, w1 * w0, w0 * w0};
     if (!fixup_nodal<9>(x, W)) return false;
-#pragma unroll
-    for (int m = 0; m < 9; ++m) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) acc = fma(cM.fwd[m][k], x[k], acc);
-        u[m] = acc;
-    }
+    modal_forward(x, u);
     return true;
 }
 

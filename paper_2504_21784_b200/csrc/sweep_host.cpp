@@ -231,6 +231,10 @@ static bool build_modal(ModalConsts& mc, std::string& err) {
         mc.V1re[a] = V[a][1].real();
         mc.V1im[a] = V[a][1].imag();
     }
+    for (int a = 0; a < 3; ++a) {
+        mc.V1re2[a] = 2.0 * mc.V1re[a];
+        mc.V1im2n[a] = -2.0 * mc.V1im[a];
+    }
     mc.V1re2x = 2.0 * mc.V1re[2];
     mc.V1im2x = 2.0 * mc.V1im[2];
     // 9x9 real maps; modal reals m = [u00, u01r, u01i, u10r, u10i, u11r, u11i, u12r, u12i]
