@@ -366,6 +366,9 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 #ifndef SWEEP_ROWS_P1K1
 #define SWEEP_ROWS_P1K1 4  // C3: 0.53 -> 0.34 ms vs 8 rows; C4 unchanged (round-1 sweep of 2-16 rows x 2-8 columns)
 #endif
+#ifndef SWEEP_ROWS_P2K1
+#define SWEEP_ROWS_P2K1 4  // experiment builds: 2 rows with 8 columns (column loop) hit an illegal instruction, untriaged
+#endif
 #ifndef SWEEP_COLS_K1
 #define SWEEP_COLS_K1 4
 #endif
@@ -373,7 +376,7 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 #define SWEEP_ROWS_K4 2
 #endif
 __host__ __device__ constexpr int rows_per_strip(int P, int K) {
-    return K >= 4 ? SWEEP_ROWS_K4 : (K == 2 ? 4 : (P == 2 ? 4 : SWEEP_ROWS_P1K1));
+    return K >= 4 ? SWEEP_ROWS_K4 : (K == 2 ? 4 : (P == 2 ? SWEEP_ROWS_P2K1 : SWEEP_ROWS_P1K1));
 }
 #ifndef SWEEP_COLS_K4
 #define SWEEP_COLS_K4 8
@@ -470,7 +473,10 @@ __device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc,
 // OPT bits (compile time): OPT_SIGMA appends sum_g sigma_g (phi, J) (NEXT-1), OPT_FIXUP
 // applies the zero-and-scale fixup to every element solve (NEXT-2).
 template <int P, int LOG2LG, int K, int OPT>
-__global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sweep2DParams prm) {
+#ifndef SWEEP_K1_MINB
+#define SWEEP_K1_MINB 1
+#endif
+__global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1))) sweep2d_kernel(const Sweep2DParams prm) {
     constexpr bool SIG = (OPT & OPT_SIGMA) != 0;
     constexpr bool FIX = (OPT & OPT_FIXUP) != 0;
     constexpr int NP1 = P + 1;
@@ -764,6 +770,93 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : 1)) sweep2d_kernel(const Sw
 #define SWEEP_COL_UNROLL 1
 #endif
             constexpr int kColUnroll = SWEEP_COL_UNROLL;
+#ifndef SWEEP_SKEW_K1
+#define SWEEP_SKEW_K1 1
+#endif
+            if constexpr (K == 1 && LG == 1 && SWEEP_SKEW_K1 && !FIX) {
+                // one group per direction (C3): a lane has a single solve chain per element,
+                // so the chunk is swept along its anti-diagonals (element (r, col) needs only
+                // (r - 1, col) and (r, col - 1)); the up to min(T, C) solves of a diagonal
+                // are independent and the fully unrolled code interleaves them.  The
+                // y-traces of all C columns are loaded up front (one L2 round trip per chunk).
+                // Measured: C3 0.349 -> 0.321 ms; with a group reduction per element (LG > 1:
+                // C4, the 8- and 16-group ranks of C5) it was 3-16 % slower, so those keep
+                // the column loop.
+                double tyc[C][NT];
+                if (J == 0) {
+#pragma unroll
+                    for (int col = 0; col < C; ++col) {
+                        const int ipc = i0 + col;
+                        const int i = fx ? nx - 1 - ipc : ipc;
+                        const bool on = ipc < nx && gl < sd.ng;
+                        double t[NP1];
+#pragma unroll
+                        for (int aq = 0; aq < NP1; ++aq) {
+                            const int a = fx ? P - aq : aq;
+                            t[aq] = on ? prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + sd.g0 + gl] : 0.0;
+                        }
+                        if constexpr (P == 2) {
+                            tyc[col][0] = cM.W0[0] * t[0] + cM.W0[1] * t[1] + cM.W0[2] * t[2];
+                            tyc[col][1] = cM.W1re[0] * t[0] + cM.W1re[1] * t[1] + cM.W1re[2] * t[2];
+                            tyc[col][2] = cM.W1im[0] * t[0] + cM.W1im[1] * t[1] + cM.W1im[2] * t[2];
+                        } else {
+                            tyc[col][0] = t[0];
+                            tyc[col][1] = t[1];
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int col = 0; col < C; ++col)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            tyc[col][t] = ld_hint(ysrc + (size_t)(i0 + col) * NT * NL + t * NL + tid, pol_last);
+                }
+#pragma unroll
+                for (int dg = 0; dg < T + C - 1; ++dg) {
+#pragma unroll
+                    for (int r = 0; r < T; ++r) {
+                        const int col = dg - r;
+                        if (col < 0 || col >= C) continue;
+                        const int el = col * T + r;
+                        double qh[NQ], u[NQ], txo[NT], tyo[NT];
+#pragma unroll
+                        for (int m = 0; m < NQ; ++m) qh[m] = qs[((size_t)el * NN + m) * GBK + gl];
+                        const double st = ss[el * GBK + gl];
+                        if constexpr (P == 2) solve_p2(L, st, qh, tx[0][r], tyc[col], u, txo, tyo);
+                        else solve_p1(L, st, qh, tx[0][r], tyc[col], u, txo, tyo);
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            tx[0][r][t] = txo[t];
+                            tyc[col][t] = tyo[t];
+                        }
+                        double* Sd = S + (size_t)el * SEL + dl * NQ;
+                        if constexpr (SIG) {
+                            double us[2 * NQ];
+#pragma unroll
+                            for (int m = 0; m < NQ; ++m) {
+                                us[m] = u[m];
+                                us[NQ + m] = st * u[m];
+                            }
+                            double* Sd2 = S2 + (size_t)el * SEL + dl * NQ;
+                            auto sink = [&](int idx, double val) {
+                                if (idx < NQ) Sd[idx] = val;
+                                else Sd2[idx - NQ] = val;
+                            };
+                            ReduceScatter<2 * NQ, LG / 2>::run(us, lane, 0, 2 * NQ, sink);
+                        } else {
+                            auto sink = [&](int idx, double val) { Sd[idx] = val; };
+                            ReduceScatter<NQ, LG / 2>::run(u, lane, 0, NQ, sink);
+                        }
+                    }
+                }
+                if (write_y) {
+#pragma unroll
+                    for (int col = 0; col < C; ++col)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            st_hint(ydst + (size_t)(i0 + col) * NT * NL + t * NL + tid, tyc[col][t], pol_last);
+                }
+            } else
 #pragma unroll kColUnroll
             for (int col = 0; col < C; ++col) {
                 const int ip = i0 + col;

@@ -1,5 +1,5 @@
 """Timeline of the persistent 2-D sweep: per task start/end/wait (trace build).
-usage: python profiles/trace_tasks.py [cfg]"""
+usage: python profiles/trace_tasks.py [cfg] [G_loc]   (G_loc: the first G_loc groups, a group-sharded rank)"""
 import ctypes
 import os
 import subprocess
@@ -20,6 +20,9 @@ B.build(extra=["-DSWEEP_TRACE"], out=so)
 S._lib = None
 lib = S.load_library(so)
 prob = synth.config(cfg)
+if len(sys.argv) > 2:
+    prob = prob.group_slice(0, int(sys.argv[2]))
+    prob.q, prob.sigma, prob.inflow = (np.ascontiguousarray(x) for x in (prob.q, prob.sigma, prob.inflow))
 dev = torch.device("cuda:0")
 sig, q, fl = (torch.from_numpy(a).to(dev) for a in (prob.sigma, prob.q, prob.inflow))
 sw = S.from_problem(prob)
