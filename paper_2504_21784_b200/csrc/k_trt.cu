@@ -15,47 +15,49 @@ namespace sweepk {
 
 constexpr double K15_PI4 = 0.15398973382026503;  // 15 / pi^4
 
-// int_0^x t^3/(e^t-1) dt * 15/pi^4 and its derivative (15/pi^4) x^3/(e^x-1)
-__device__ __forceinline__ void planck_P(double x, double& P, double& dP) {
+// int_0^x t^3/(e^t-1) dt * 15/pi^4, its derivative (15/pi^4) x^3/(e^x-1) and 1/(e^x-1)
+__device__ __forceinline__ void planck_P(double x, double& P, double& dP, double& rem1) {
     if (!(x > 0.0)) {
         P = 0.0;
         dP = 0.0;
+        rem1 = 0.0;
         return;
     }
     const double x2 = x * x, x3 = x2 * x;
-    dP = K15_PI4 * x3 / expm1(x);
-    if (x < 1.5) {
+    rem1 = 1.0 / expm1(x);
+    dP = K15_PI4 * x3 * rem1;
+    if (x < 3.0) {
         // Bernoulli series sum_k B_k x^(k+3) / (k! (k+3)) (|x| < 2 pi): x^3/3 - x^4/8 +
-        // sum_j c_j x^(2j+3), c_j = B_2j / ((2j)! (2j+3)), j = 1..12 (Horner in x^2)
-        const double c[13] = {1.0 / 3.0,
-                              1.0 / 60.0,                    // B2/(2! 5)
-                              -1.0 / 5040.0,                 // B4/(4! 7)
-                              1.0 / 272160.0,                // B6/(6! 9)
-                              -1.0 / 13305600.0,             // B8/(8! 11)
-                              1.0 / 622702080.0,             // B10/(10! 13)
-                              -691.0 / (2730.0 * 479001600.0 * 15.0),
-                              7.0 / (6.0 * 87178291200.0 * 17.0),
-                              -3617.0 / (510.0 * 20922789888000.0 * 19.0),
-                              43867.0 / (798.0 * 6402373705728000.0 * 21.0),
-                              -174611.0 / (330.0 * 2432902008176640000.0 * 23.0),
-                              854513.0 / (138.0 * 1.1240007277776077e21 * 25.0),
-                              -236364091.0 / (2730.0 * 6.204484017332394e23 * 27.0)};
-        double s = c[12];
+        // sum_j c_j x^(2j+3), c_j = B_2j / ((2j)! (2j+3)), j = 1..25 (Horner in x^2; the
+        // j = 25 term is below 1e-16 of the sum at x = 3).  Exact Bernoulli numbers,
+        // rounded once to double (hex literals).  The switch at x = 3 (not 1.5) cuts the
+        // tail loop below from 27 to 14 terms; a warp's lanes straddle the switch, so
+        // both branches are paid.
+        constexpr double c[26] = {1.0 / 3.0,
+                                  0x1.1111111111111p-6,  -0x1.a01a01a01a01ap-13, 0x1.ed284dc73b445p-19,
+                                  -0x1.42cb40df7f3abp-24, 0x1.b96d79892884cp-30, -0x1.35de417c02910p-35,
+                                  0x1.bb28a22b53d89p-41,  -0x1.41626d7230484p-46, 0x1.d762338fbb4bfp-52,
+                                  -0x1.5cdcee4b98370p-57, 0x1.0427c1f1c4c70p-62, -0x1.8681da5029235p-68,
+                                  0x1.26b40ee19058bp-73,  -0x1.beeea26d5ca6ap-79, 0x1.5450579047e7ap-84,
+                                  -0x1.0415d3bd22f20p-89, 0x1.8ed7e280fa8fbp-95, -0x1.32b61253f8daap-100,
+                                  0x1.d8f77f88e815cp-106, -0x1.6d8a89aff8a6ap-111, 0x1.1b20b5bdfa81ap-116,
+                                  -0x1.b7753eeb0a071p-122, 0x1.55ac07fbb064ep-127, -0x1.0a1690e38bf07p-132,
+                                  0x1.9f1680b3fee0ep-138};
+        double s = c[25];
 #pragma unroll
-        for (int j = 11; j >= 1; --j) s = fma(s, x2, c[j]);
+        for (int j = 24; j >= 1; --j) s = fma(s, x2, c[j]);
         // sum = x^3 [1/3 - x/8 + x^2 (c1 + x^2 (c2 + ...))]
-        const double even = fma(s, x2, 0.0);
-        P = K15_PI4 * x3 * (c[0] - x * 0.125 + even);
+        P = K15_PI4 * x3 * (c[0] - x * 0.125 + s * x2);
     } else {
         // 1 - (15/pi^4) sum_n e^{-n x} (x^3/n + 3x^2/n^2 + 6x/n^3 + 6/n^4); terms until
-        // e^{-n x} < e^{-38} (x >= 1.5: at most 27), 1/n from an unrolled table
+        // e^{-n x} < e^{-38} (x >= 3: at most 14), 1/n from an unrolled table
         double tail = 0.0;
         const double e1 = exp(-x);
         double en = 1.0;
         const int nmax = (int)(38.0 / x) + 2;
         const double x6 = 6.0 * x, x23 = 3.0 * x2;
 #pragma unroll
-        for (int n = 1; n <= 27; ++n) {
+        for (int n = 1; n <= 14; ++n) {
             if (n > nmax) break;
             const double rn = 1.0 / (double)n;  // folded to a constant (unrolled)
             en *= e1;
@@ -83,11 +85,11 @@ __global__ void trt_emission_kernel(const double* __restrict__ T, const double* 
         const int g = (int)(ii - v * G);
         const double t = T[v];
         const double it = 1.0 / t;
-        double Pr, d;
-        planck_P(nu[g + 1] * it, Pr, d);
+        double Pr, d, d2;
+        planck_P(nu[g + 1] * it, Pr, d, d2);
         double Pl = __shfl_up_sync(0xffffffffu, Pr, 1);
         const double lo_from_left = __shfl_up_sync(0xffffffffu, (double)v, 1);
-        if (g == 0 || lane == 0 || lo_from_left != (double)v) planck_P(nu[g] * it, Pl, d);
+        if (g == 0 || lane == 0 || lo_from_left != (double)v) planck_P(nu[g] * it, Pl, d, d2);
         if (on) {
             const size_t e = v / n;
             const double t2 = t * t;
@@ -96,45 +98,55 @@ __global__ void trt_emission_kernel(const double* __restrict__ T, const double* 
     }
 }
 
-// sum_g sig_g B_g(T) and its T-derivative over the groups, one warp per node: lane l
-// evaluates P at the bounds b = l, l + 32, ... and owns group g = b - 1 (its lower bound
-// comes from the neighbouring lane, or from lane 31 of the previous round); fixed-order
-// butterfly sums, so every lane ends with the same E, dE
+// sum_g sig_g B_g(T) and its first two T-derivatives over the groups, one warp per node:
+// lane l evaluates P at the bounds b = l, l + 32, ... and owns group g = b - 1 (its lower
+// bound comes from the neighbouring lane, or from lane 31 of the previous round);
+// fixed-order butterfly sums, so every lane ends with the same E, dE, d2E.  With
+// B(T) = T^4 P(nu/T), x = nu/T, h = x P'(x), q = x h e^x/(e^x - 1):
+//   dB/dT = T^3 (4P - h),   d2B/dT2 = T^2 (12P - 3h - q).
 __device__ __forceinline__ void emission_sum_warp(double T, int G, const double* __restrict__ sig,
-                                                  const double* __restrict__ nu, int lane, double& E, double& dE) {
-    const double T3 = T * T * T, T4 = T3 * T, iT = 1.0 / T;
-    double e = 0.0, de = 0.0;
-    double carry_P = 0.0, carry_x = 0.0, carry_dP = 0.0;  // bound 32k - 1 (lane 31 of the previous round)
+                                                  const double* __restrict__ nu, int lane, double& E, double& dE,
+                                                  double& d2E) {
+    const double T2 = T * T, T3 = T2 * T, T4 = T3 * T, iT = 1.0 / T;
+    double e = 0.0, de = 0.0, d2e = 0.0;
+    double carry_P = 0.0, carry_h = 0.0, carry_q = 0.0;  // bound 32k - 1 (lane 31 of the previous round)
     for (int b0 = 0; b0 <= G; b0 += 32) {
         const int bnd = b0 + lane;
-        double P = 0.0, dP = 0.0, x = 0.0;
+        double P = 0.0, h = 0.0, q = 0.0;
         if (bnd <= G) {
-            x = nu[bnd] * iT;
-            planck_P(x, P, dP);
+            const double x = nu[bnd] * iT;
+            double dP, rem1;
+            planck_P(x, P, dP, rem1);
+            h = x * dP;
+            q = x * h * (1.0 + rem1);
         }
-        double Pl = __shfl_up_sync(0xffffffffu, P, 1), dPl = __shfl_up_sync(0xffffffffu, dP, 1),
-               xl = __shfl_up_sync(0xffffffffu, x, 1);
+        double Pl = __shfl_up_sync(0xffffffffu, P, 1), hl = __shfl_up_sync(0xffffffffu, h, 1),
+               ql = __shfl_up_sync(0xffffffffu, q, 1);
         if (lane == 0) {
             Pl = carry_P;
-            dPl = carry_dP;
-            xl = carry_x;
+            hl = carry_h;
+            ql = carry_q;
         }
         if (bnd >= 1 && bnd <= G) {
             const double sg = sig[bnd - 1];
-            e = fma(sg, T4 * (P - Pl), e);
-            de = fma(sg, T3 * (4.0 * (P - Pl) - (x * dP - xl * dPl)), de);
+            const double dPg = P - Pl, dhg = h - hl, dqg = q - ql;
+            e = fma(sg, T4 * dPg, e);
+            de = fma(sg, T3 * (4.0 * dPg - dhg), de);
+            d2e = fma(sg, T2 * (12.0 * dPg - 3.0 * dhg - dqg), d2e);
         }
         carry_P = __shfl_sync(0xffffffffu, P, 31);
-        carry_dP = __shfl_sync(0xffffffffu, dP, 31);
-        carry_x = __shfl_sync(0xffffffffu, x, 31);
+        carry_h = __shfl_sync(0xffffffffu, h, 31);
+        carry_q = __shfl_sync(0xffffffffu, q, 31);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         e += __shfl_xor_sync(0xffffffffu, e, o);
         de += __shfl_xor_sync(0xffffffffu, de, o);
+        d2e += __shfl_xor_sync(0xffffffffu, d2e, o);
     }
     E = e;
     dE = de;
+    d2E = d2e;
 }
 
 // per node (one warp): solve cv_dt (T - Tk) + E(T) = sphi by a bracketed Newton
@@ -157,8 +169,8 @@ __global__ void __launch_bounds__(256) trt_update_kernel(const double* __restric
         double lo = 0.0, hi = -1.0;  // hi < 0: no upper bracket yet
         bool ok = false;
         for (int it = 0; it < 100; ++it) {
-            double E, dE;
-            emission_sum_warp(t, G, sg, nu, lane, E, dE);
+            double E, dE, d2E;
+            emission_sum_warp(t, G, sg, nu, lane, E, dE, d2E);
             const double f = fma(cv_dt, t - tk, E - s);
             // converged to the rounding noise of f (a few ulps of its largest term): a Newton
             // step from here would only chase that noise (and fall back to bisection)
@@ -168,20 +180,34 @@ __global__ void __launch_bounds__(256) trt_update_kernel(const double* __restric
             }
             if (f < 0.0) lo = t;
             else hi = t;
-            // Newton step in v = T^m, m = t E'/E the local power-law exponent of the
-            // emission: exact in one step for a single power law, so cooling nodes whose
-            // root lies far below T (emission ~ T^4 >> the absorbed sphi) do not creep down
-            // by the factor 3/4 per step plain Newton would take; to first order it is the
-            // plain Newton step T - f/f'
+            // far from the root: Newton step in v = T^m, m = t E'/E the local power-law
+            // exponent of the emission: exact in one step for a single power law, so cooling
+            // nodes whose root lies far below T (emission ~ T^4 >> the absorbed sphi) do not
+            // creep down by the factor 3/4 per step plain Newton would take.  Close to it
+            // (Newton step below 5 %): Halley's step (cubic convergence), which ends the
+            // iteration one evaluation earlier than Newton's on most nodes.
             const double fp = cv_dt + dE;
-            const double m = (E > 0.0) ? fmax(1.0, t * dE / E) : 1.0;
-            const double r = 1.0 - m * f / (t * fp);
-            double tn = (r > 0.0) ? t * exp(log(r) / m) : 0.0;  // 0: rejected by the bracket below
-            if (!(tn > lo) || (hi > 0.0 && !(tn < hi))) tn = (hi > 0.0) ? 0.5 * (lo + hi) : 2.0 * t;
-            // converged: a step below 1e-13 relative (the iterate after it is exact to rounding:
-            // quadratic convergence; smaller thresholds sit below the rounding noise of f), or
-            // the sign bracket that narrow
-            const bool done = fabs(tn - t) <= 1e-13 * tn || (hi > 0.0 && hi - lo <= 1e-15 * hi);
+            const double nr = f / (t * fp);
+            double tn;
+            bool halley = false;
+            if (fabs(nr) < 0.05) {
+                const double den = 2.0 * fp * fp - f * d2E;
+                halley = den > 0.0;
+                tn = halley ? t - 2.0 * f * fp / den : t - f / fp;
+            } else {
+                const double m = (E > 0.0) ? fmax(1.0, t * dE / E) : 1.0;
+                const double r = 1.0 - m * nr;
+                tn = (r > 0.0) ? t * exp(log(r) / m) : 0.0;  // 0: rejected by the bracket below
+            }
+            if (!(tn > lo) || (hi > 0.0 && !(tn < hi))) {
+                tn = (hi > 0.0) ? 0.5 * (lo + hi) : 2.0 * t;
+                halley = false;
+            }
+            // converged: a Halley step below 1e-7 relative (the error after it is of the
+            // order of its cube), a Newton step below 1e-13 (the iterate after it is exact to
+            // rounding: quadratic convergence; smaller thresholds sit below the rounding noise
+            // of f), or the sign bracket that narrow
+            const bool done = fabs(tn - t) <= (halley ? 1e-7 : 1e-13) * tn || (hi > 0.0 && hi - lo <= 1e-15 * hi);
             t = tn;
             if (done) {
                 ok = true;
