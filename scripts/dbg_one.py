@@ -5,7 +5,7 @@ from synth.configs import random_problem
 import paper_2504_21784_b200 as pk
 from tests.parity import field_errors
 nx, ny, p, nd, G = map(int, sys.argv[1:6])
-prob = random_problem(507, 2, nx, ny, p, nd, G)
+prob = random_problem(int(os.environ.get("SEED", 507)), 2, nx, ny, p, nd, G)
 try:
     got = pk.run_problem(prob)
     ref = oracle.sweep(prob)
