@@ -44,7 +44,7 @@ def flops_per_edg(p: int, dim: int, n_dir_quad: int, gb: int) -> float:
     """Flops per (element, distinct direction, group) of the implemented algorithm
     (FMA = 2, reciprocal = 1), counted from the kernel source."""
     if dim == 2 and p == 2:
-        solve = 52 + 11 + 13 + 33 + 38           # lifts, shifts, reciprocals, scaling, traces
+        solve = 52 + 11 + 13 + 33 + 11           # lifts, shifts, reciprocals, scaling, traces
         group_sum = 9                             # sum over groups of the 9 modal values
         q_transform = 2 * 81 / n_dir_quad         # modal transform of q per (e, g), per quadrant
         moments = 2 * (6 * 9 + 6 * 81 / n_dir_quad) / gb

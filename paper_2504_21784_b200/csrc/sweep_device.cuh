@@ -219,17 +219,17 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     traces_p2(u, txo, tyo);
 }
 
-// outflow traces of a modal element solution: x+ face (y-modal), y+ face (x-modal)
+// outflow traces of a modal element solution: x+ face (y-modal), y+ face (x-modal).
+// The eigenvectors are scaled to 1 at the outflow node (build_modal), so a trace is
+// the sum of the modal coefficients along the other axis: 9 adds instead of 22 ops.
 __device__ __forceinline__ void traces_p2(const double (&u)[9], double (&txo)[3], double (&tyo)[3]) {
-    const double v0 = cM.V0[2], vr = cM.V1re[2], vi = cM.V1im[2], vr2 = cM.V1re2x, vi2 = cM.V1im2x;
-    const double sr = u[5] + u[7], dr = u[5] - u[7];
-    const double si = u[6] + u[8], di = u[6] - u[8];
-    txo[0] = v0 * u[0] + vr2 * u[3] - vi2 * u[4];
-    txo[1] = v0 * u[1] + vr * sr - vi * si;
-    txo[2] = v0 * u[2] + vr * di + vi * dr;
-    tyo[0] = v0 * u[0] + vr2 * u[1] - vi2 * u[2];
-    tyo[1] = v0 * u[3] + vr * sr - vi * di;
-    tyo[2] = v0 * u[4] + vr * si + vi * dr;
+    const double sr = u[5] + u[7];
+    txo[0] = fma(2.0, u[3], u[0]);
+    txo[1] = u[1] + sr;
+    txo[2] = u[2] + (u[6] - u[8]);
+    tyo[0] = fma(2.0, u[1], u[0]);
+    tyo[1] = u[3] + sr;
+    tyo[2] = u[4] + (u[6] + u[8]);
 }
 
 // q^ = (W (x) W) q in the 9 modal reals, factored: W along x for each y-row,
@@ -422,39 +422,65 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// L2 eviction-priority policies: streamed inputs are evict-first (each quadrant
-// re-reads them much later), the strip-boundary trace ring is evict-last (read
-// back by the next strip soon).
-__device__ __forceinline__ unsigned long long policy_evict_first() {
-    unsigned long long p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_last() {
-    unsigned long long p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
+// L2 eviction-priority policy for the streamed inputs: evict-first (each quadrant
+// re-reads them much later), created inside the copy's own asm block.  The
+// strip-boundary trace ring uses plain loads and stores: an evict-last policy there
+// (kept in a register through the whole persistent kernel, or created per access)
+// gained nothing measurable and coincided with "illegal instruction" faults in some
+// register allocations of the one-group-per-lane p = 2 kernels; it is kept behind
+// SWEEP_L2HINT_RING for experiments.  The pol arguments document the intended policy.
+__device__ __forceinline__ unsigned long long policy_evict_first() { return 0ull; }
+__device__ __forceinline__ unsigned long long policy_evict_last() { return 1ull; }
 __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
-                                              unsigned long long pol) {
+                                              unsigned long long) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}" ::"r"(
             smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#ifdef SWEEP_L2HINT_RING
+__device__ __forceinline__ void st_hint(double* p, double v, unsigned long long) {
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "st.global.L2::cache_hint.f64 [%0], %1, pol;\n\t}" ::"l"(p),
+        "d"(v)
+        : "memory");
 }
-__device__ __forceinline__ double ld_hint(const double* p, unsigned long long pol) {
+__device__ __forceinline__ double ld_hint(const double* p, unsigned long long) {
     double v;
-    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "ld.global.cg.L2::cache_hint.f64 %0, [%1], pol;\n\t}"
+        : "=d"(v)
+        : "l"(p)
+        : "memory");
     return v;
 }
-__device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc, unsigned long long pol) {
+__device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc, unsigned long long) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "l"(pol) : "memory");
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, pol;\n\t}" ::"r"(d),
+        "l"(gsrc)
+        : "memory");
 }
+#else
+__device__ __forceinline__ void st_hint(double* p, double v, unsigned long long) {
+    asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_hint(const double* p, unsigned long long) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc, unsigned long long) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+#endif
 
 // Lane layout: LG = 2^LOG2LG consecutive lanes share one direction and hold
 // consecutive groups; each lane carries K groups (g, g + LG, ...), so a stream

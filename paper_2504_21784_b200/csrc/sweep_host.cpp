@@ -192,6 +192,17 @@ static bool build_modal(ModalConsts& mc, std::string& err) {
         const cplx ph = std::abs(V[im][0]) / V[im][0];
         for (int a = 0; a < 3; ++a) V[a][0] = cplx((V[a][0] * ph).real(), 0.0);
     }
+    // scale each eigenvector to 1 at the outflow node (a = 2): the outflow traces of a
+    // modal solution are then plain sums of modal coefficients (traces_p2)
+    for (int k = 0; k < 2; ++k) {
+        const cplx piv = V[2][k];
+        if (!(std::abs(piv) > 1e-3)) {
+            err = "modal: eigenvector vanishes at the outflow node";
+            return false;
+        }
+        for (int a = 0; a < 2; ++a) V[a][k] /= piv;
+        V[2][k] = cplx(1.0, 0.0);
+    }
     for (int a = 0; a < 3; ++a) V[a][2] = std::conj(V[a][1]);
     // W = V^-1 (adjugate)
     cplx detV = V[0][0] * (V[1][1] * V[2][2] - V[1][2] * V[2][1]) - V[0][1] * (V[1][0] * V[2][2] - V[1][2] * V[2][0]) +
@@ -235,8 +246,6 @@ static bool build_modal(ModalConsts& mc, std::string& err) {
         mc.V1re2[a] = 2.0 * mc.V1re[a];
         mc.V1im2n[a] = -2.0 * mc.V1im[a];
     }
-    mc.V1re2x = 2.0 * mc.V1re[2];
-    mc.V1im2x = 2.0 * mc.V1im[2];
     // 9x9 real maps; modal reals m = [u00, u01r, u01i, u10r, u10i, u11r, u11i, u12r, u12i]
     const int pairs[5][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {1, 2}};
     for (int k = 0; k < 9; ++k) {

@@ -36,8 +36,7 @@ struct ModalConsts {
     double W0[3];          // real row of W
     double W1re[3], W1im[3];
     double V0[3];          // real column of V (V[a][0])
-    double V1re[3], V1im[3];   // V[a][1]
-    double V1re2x, V1im2x;     // 2 V[2][1] (outflow traces)
+    double V1re[3], V1im[3];   // V[a][1]  (V[2][0] = V[2][1] = 1: scaled at the outflow node)
     double V1re2[3], V1im2n[3];  // 2 Re V[a][1], -2 Im V[a][1] (separable modal -> nodal map)
     // real 9x9 maps between nodal (k = a + 3b, sweep coordinates) and the 9 modal
     // reals m = [u00, u01r, u01i, u10r, u10i, u11r, u11i, u12r, u12i]

@@ -31,9 +31,9 @@ def test_roofline_model():
     sys.path.insert(0, ROOT)
     import bench
     import synth
-    # C5: 171.4 flops per (element, distinct direction, group) with 16 directions per quadrant
+    # C5: 144.4 flops per (element, distinct direction, group) with 16 directions per quadrant
     f = bench.flops_per_edg(2, 2, 16, 32)
-    assert 165 < f < 180
+    assert 140 < f < 150
     prob = synth.config(1)
     assert bench.algorithmic_bytes(prob) == 8 * (prob.sigma.size + prob.q.size + prob.inflow.size +
                                                  prob.n_el * prob.n * 3 + 2 * prob.n_bnode)
