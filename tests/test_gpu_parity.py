@@ -243,3 +243,16 @@ def test_nccl_allreduce_plumbing_one_rank(lib, monkeypatch):
         kt = sw.kernel_times(3)
     assert np.array_equal(got, plain)
     assert (kt[:, 2] >= 0).all()
+
+
+# Every 2-D lane layout (groups per lane K, lanes per direction LG; chosen from G) on
+# narrow meshes with several strips (ny > rows per strip): the pattern of layouts and
+# shapes under which one code-generation of the p = 2 one-group-per-lane kernels once
+# faulted (profiles/r01_ncu_c5_sweep2d.md).
+LAYOUTS = [(p, G, nx, ny) for p in (1, 2) for G in (1, 2, 5, 8, 16, 33, 64) for nx, ny in ((1, 7), (2, 9), (5, 13))]
+
+
+@pytest.mark.parametrize("p,G,nx,ny", LAYOUTS)
+def test_layout_matrix(lib, p, G, nx, ny):
+    prob = random_problem(700 + 10 * G + nx, 2, nx, ny, p, 8, G)
+    check(lib, prob)
