@@ -53,10 +53,11 @@ def planck_series(x: float, c) -> float:
     return 15 / math.pi ** 4 * x ** 3 * (c[0] - x * 0.125 + s * x2)
 
 
-def planck_tail(x: float) -> float:
+def planck_tail(x: float, full: bool = False) -> float:
+    # the kernel's x >= switch branch (full: 80 terms, the reference for both branches)
     t = 0.0
     en, e1 = 1.0, math.exp(-x)
-    for n in range(1, min(14, int(38.0 / x) + 2) + 1):
+    for n in range(1, (80 if full else min(14, int(38.0 / x) + 2)) + 1):
         rn = 1.0 / n
         en *= e1
         t += en * rn * (rn * (rn * (6 * rn + 6 * x) + 3 * x * x) + x ** 3)
@@ -69,9 +70,12 @@ def test_series_and_tail_agree_at_the_switch():
     _, c = table()
     src = open(SRC).read()
     assert "if (x < 3.0)" in src
-    for x in (2.0, 2.5, 2.9, 3.0):
-        a, b = planck_series(x, c), planck_tail(x)
+    for x in (1.0, 2.0, 2.5, 2.9, 2.999):
+        a, b = planck_series(x, c), planck_tail(x, full=True)
         assert abs(a - b) <= 4e-15 * b, (x, a, b)
+    for x in (3.0, 3.5, 5.0, 12.0, 40.0):
+        a, b = planck_tail(x), planck_tail(x, full=True)
+        assert abs(a - b) <= 1e-16 * b, (x, a, b)
 
 
 def test_planck_limits():
