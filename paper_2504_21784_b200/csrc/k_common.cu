@@ -209,7 +209,12 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
     const int T = rows_per_strip(p, k), C = cols_per_chunk(p, k, opt), NQ = nq_of(p), NN = (p + 1) * (p + 1);
     const int CT = C * T;
     const int NL = dset * gbk / k;  // threads per CTA
-    const int s2 = (opt & OPT_SIGMA) ? CT * (dset * NQ + 1) : 0;
+#ifndef SWEEP_DEFER_C
+#define SWEEP_DEFER_C 1
+#endif
+    // sigma moments: S2; otherwise (DEFER, not for one group per direction) a second S buffer
+    const bool defer = SWEEP_DEFER_C && !(k == 1 && gbk == 1);
+    const int s2 = ((opt & OPT_SIGMA) || defer) ? CT * (dset * NQ + 1) : 0;
     return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + 81 + s2) *
            (int)sizeof(double);
 }

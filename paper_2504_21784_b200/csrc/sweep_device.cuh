@@ -634,6 +634,15 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         constexpr int NFO = SIG ? 9 : 6;       // node fields: 6 moments (+ sigma phi, sigma Jx, sigma Jy)
         double* bckS = ypre + K * NT * NL;     // [9][9] modal -> nodal (p = 2, boundary closures)
         double* S2 = bckS + 81;                // SIG: [CT][SEL] sigma-weighted group sums
+#ifndef SWEEP_DEFER_C
+#define SWEEP_DEFER_C 1
+#endif
+        // DEFER: phase C of chunk c-1 runs while thread 0 waits for the strip below to
+        // release chunk c, so S is double-buffered (C5 11.70 -> 11.55 ms).  Not with the
+        // sigma moments (S2 would need a second buffer too, past the shared-memory
+        // limit) and not for one group per direction (C3: 0.324 -> 0.347 ms)
+        constexpr bool DEFER = SWEEP_DEFER_C && !SIG && !(K == 1 && LG == 1);
+        double* Salt = S2 + (SIG ? (size_t)CT * SEL : 0);  // DEFER: S of the odd chunks
         const size_t sig_off = 6 * nodes + 2 * (size_t)prm.nbnode;  // SIG: sigma phi | sigma J
         // (compile-time constant-bank indices only: ptxas hoists constant loads out of
         // the task loop for every thread, and a thread-dependent index past the end of
@@ -685,9 +694,122 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             }
         }
 
+        // ---- phase C: sum over the CTA's directions with the moment / boundary
+        // weights, back to nodal values, write this stream's slab.
+        // stage 1: M[el][f][m] = sum_d coef[d][f] S[el][d][m] for the 6 moment fields,
+        //          one output per thread and pass (consecutive threads: consecutive m);
+        //          boundary fields (beta, J+) per (element, face) on boundary elements;
+        // stage 2 (p = 2): nodal psi[el][f][k] = sum_m bck[k][m] M[el][f][m].
+        auto phase_c = [&](const int i0, const int cols, const double* S) {
+#ifndef SWEEP_ABL_NOPHASEC
+                auto node_store = [&](double* dst, int kk, double v) {
+                    const int aq = kk % NP1, bq = kk / NP1;
+                    const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
+                    dst[a + NP1 * b] = v;
+                };
+                // field f < 6: the moments from S; SIG f = 6, 7, 8: sigma phi, sigma Jx,
+                // sigma Jy from S2 with the weights of phi, Jx, Jy
+                auto field_dst = [&](int f) -> double* {
+                    return slab + ((f < 6) ? (size_t)f * nodes : sig_off + (size_t)(f - 6) * nodes);
+                };
+                // PC outputs per thread per pass: independent accumulation chains, and all
+                // their S loads ahead of the stores (Mbuf and S share the smem window)
+#ifndef SWEEP_PC
+#define SWEEP_PC 1  // 4 (0.3 % faster at C5) hits an illegal-instruction fault in the p = 2, 2-lane layout with modal slabs
+#endif
+                constexpr int PC = SWEEP_PC;
+                for (int o0 = tid; o0 < CT * NFO * NQ; o0 += PC * NL) {
+                    const double* Sp[PC];
+                    const double* cf[PC];
+                    double acc[PC];
+#pragma unroll
+                    for (int u = 0; u < PC; ++u) {
+                        const int o = min(o0 + u * NL, CT * NFO * NQ - 1);
+                        const int m = o % NQ, rest = o / NQ;
+                        const int f = rest % NFO, el = rest / NFO;
+                        Sp[u] = ((f < 6) ? S : S2) + (size_t)el * SEL + m;
+                        cf[u] = coefS + ((f < 6) ? f : f - 6);
+                        acc[u] = 0.0;
+                    }
+                    for (int dd = 0; dd < sd.nd; ++dd) {
+#pragma unroll
+                        for (int u = 0; u < PC; ++u) acc[u] = fma(cf[u][dd * NFIELD], Sp[u][dd * NQ], acc[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < PC; ++u) {
+                        const int o = o0 + u * NL;
+                        if (o >= CT * NFO * NQ) continue;
+                        const int m = o % NQ, rest = o / NQ;
+                        const int f = rest % NFO, el = rest / NFO;
+                        const int col = el / T, r = el - col * T;
+                        if (col < cols && r < rows) {
+                            const int ip = i0 + col, jp = j0 + r;
+                            const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                            double* dst = field_dst(f) + ((size_t)i + (size_t)nx * j) * NN;
+                            // p = 2: the slab keeps the MODAL values (sweep orientation); the
+                            // finalize kernel applies each stream's back transform once per
+                            // output instead of every CTA per chunk.  p = 1: nodal already.
+                            if constexpr (P == 2) dst[m] = acc[u];
+                            else node_store(dst, m, acc[u]);
+                        }
+                    }
+                }
+                // boundary closures: (element, face) items on physical boundary faces
+                for (int o = tid; o < CT * 4; o += NL) {
+                    const int el = o >> 2, face = o & 3;
+                    const int col = el / T, r = el - col * T;
+                    if (col >= cols || r >= rows) continue;
+                    const int ip = i0 + col, jp = j0 + r;
+                    const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                    const bool on = (face == 0) ? (i == 0) : (face == 1) ? (i == nx - 1) : (face == 2) ? (j == 0) : (j == ny - 1);
+                    if (!on) continue;
+                    double Mb[NQ], Mj[NQ];
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m) Mb[m] = Mj[m] = 0.0;
+                    for (int dd = 0; dd < sd.nd; ++dd) {
+                        const double cb = coefS[dd * NFIELD + 6 + 2 * face], cj = coefS[dd * NFIELD + 7 + 2 * face];
+                        const double* Sp = S + (size_t)el * SEL + dd * NQ;
+#pragma unroll
+                        for (int m = 0; m < NQ; ++m) {
+                            Mb[m] = fma(cb, Sp[m], Mb[m]);
+                            Mj[m] = fma(cj, Sp[m], Mj[m]);
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < NP1; ++t) {
+                        int a, b, idx;
+                        if (face < 2) {
+                            a = (face == 0) ? 0 : P;
+                            b = t;
+                            idx = j;
+                        } else {
+                            b = (face == 2) ? 0 : P;
+                            a = t;
+                            idx = i;
+                        }
+                        const int kk = (fx ? P - a : a) + NP1 * (fy ? P - b : b);
+                        double vb = 0.0, vj = 0.0;
+                        if constexpr (P == 2) {
+#pragma unroll
+                            for (int m = 0; m < 9; ++m) {
+                                vb = fma(bckS[kk * 9 + m], Mb[m], vb);
+                                vj = fma(bckS[kk * 9 + m], Mj[m], vj);
+                            }
+                        } else {
+                            vb = Mb[kk];
+                            vj = Mj[kk];
+                        }
+                        const int bn = bnode2d(face, idx, t, nx, ny, NP1);
+                        slab[6 * nodes + bn] = vb;
+                        slab[6 * nodes + prm.nbnode + bn] = vj;
+                    }
+                }
+            #endif
+        };
         for (int c = 0; c < prm.n_chunks; ++c) {
             const int i0 = c * C;
             const int cols = min(C, nx - i0);
+            double* const Sc = (DEFER && (c & 1)) ? Salt : S;
             const int buf = c & 1;
             double* qs = qsb + (size_t)buf * CT * NN * GBK;
             double* ss = ssb + (size_t)buf * CT * GBK;
@@ -750,6 +872,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     }
                 }
             }
+            // DEFER: the previous chunk's direction sums while the strip below finishes
+            if constexpr (DEFER)
+                if (c > 0) phase_c(i0 - C, C, ((c - 1) & 1) ? Salt : S);
             // ---- wait until the strip below has finished this chunk
 #ifndef SWEEP_ABL_NOWAIT
             if (J > 0 && tid == 0) {
@@ -858,7 +983,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             tx[0][r][t] = txo[t];
                             tyc[col][t] = tyo[t];
                         }
-                        double* Sd = S + (size_t)el * SEL + dl * NQ;
+                        double* Sd = Sc + (size_t)el * SEL + dl * NQ;
                         if constexpr (SIG) {
                             double us[2 * NQ];
 #pragma unroll
@@ -1017,7 +1142,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             for (int m = 0; m < NQ; ++m) us[NQ + m] = (k == 0) ? st * u[m] : fma(st, u[m], us[NQ + m]);
                         }
                     }
-                    double* Sd = S + (size_t)el * SEL + dl * NQ;
+                    double* Sd = Sc + (size_t)el * SEL + dl * NQ;
                     if constexpr (SIG) {
                         double* Sd2 = S2 + (size_t)el * SEL + dl * NQ;
                         auto sink = [&](int idx, double val) {
@@ -1059,120 +1184,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             t_acc[1] += tc2 - tc1;
 #endif
 
-            // ---- phase C: sum over the CTA's directions with the moment / boundary
-            // weights, back to nodal values, write this stream's slab.
-            // stage 1: M[el][f][m] = sum_d coef[d][f] S[el][d][m] for the 6 moment fields,
-            //          one output per thread and pass (consecutive threads: consecutive m);
-            //          boundary fields (beta, J+) per (element, face) on boundary elements;
-            // stage 2 (p = 2): nodal psi[el][f][k] = sum_m bck[k][m] M[el][f][m].
-#ifdef SWEEP_ABL_NOPHASEC
-            if (false) {
-#else
-            {
-#endif
-                auto node_store = [&](double* dst, int kk, double v) {
-                    const int aq = kk % NP1, bq = kk / NP1;
-                    const int a = fx ? P - aq : aq, b = fy ? P - bq : bq;
-                    dst[a + NP1 * b] = v;
-                };
-                // field f < 6: the moments from S; SIG f = 6, 7, 8: sigma phi, sigma Jx,
-                // sigma Jy from S2 with the weights of phi, Jx, Jy
-                auto field_dst = [&](int f) -> double* {
-                    return slab + ((f < 6) ? (size_t)f * nodes : sig_off + (size_t)(f - 6) * nodes);
-                };
-                // PC outputs per thread per pass: independent accumulation chains, and all
-                // their S loads ahead of the stores (Mbuf and S share the smem window)
-#ifndef SWEEP_PC
-#define SWEEP_PC 1  // 4 (0.3 % faster at C5) hits an illegal-instruction fault in the p = 2, 2-lane layout with modal slabs
-#endif
-                constexpr int PC = SWEEP_PC;
-                for (int o0 = tid; o0 < CT * NFO * NQ; o0 += PC * NL) {
-                    const double* Sp[PC];
-                    const double* cf[PC];
-                    double acc[PC];
-#pragma unroll
-                    for (int u = 0; u < PC; ++u) {
-                        const int o = min(o0 + u * NL, CT * NFO * NQ - 1);
-                        const int m = o % NQ, rest = o / NQ;
-                        const int f = rest % NFO, el = rest / NFO;
-                        Sp[u] = ((f < 6) ? S : S2) + (size_t)el * SEL + m;
-                        cf[u] = coefS + ((f < 6) ? f : f - 6);
-                        acc[u] = 0.0;
-                    }
-                    for (int dd = 0; dd < sd.nd; ++dd) {
-#pragma unroll
-                        for (int u = 0; u < PC; ++u) acc[u] = fma(cf[u][dd * NFIELD], Sp[u][dd * NQ], acc[u]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < PC; ++u) {
-                        const int o = o0 + u * NL;
-                        if (o >= CT * NFO * NQ) continue;
-                        const int m = o % NQ, rest = o / NQ;
-                        const int f = rest % NFO, el = rest / NFO;
-                        const int col = el / T, r = el - col * T;
-                        if (col < cols && r < rows) {
-                            const int ip = i0 + col, jp = j0 + r;
-                            const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                            double* dst = field_dst(f) + ((size_t)i + (size_t)nx * j) * NN;
-                            // p = 2: the slab keeps the MODAL values (sweep orientation); the
-                            // finalize kernel applies each stream's back transform once per
-                            // output instead of every CTA per chunk.  p = 1: nodal already.
-                            if constexpr (P == 2) dst[m] = acc[u];
-                            else node_store(dst, m, acc[u]);
-                        }
-                    }
-                }
-                // boundary closures: (element, face) items on physical boundary faces
-                for (int o = tid; o < CT * 4; o += NL) {
-                    const int el = o >> 2, face = o & 3;
-                    const int col = el / T, r = el - col * T;
-                    if (col >= cols || r >= rows) continue;
-                    const int ip = i0 + col, jp = j0 + r;
-                    const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
-                    const bool on = (face == 0) ? (i == 0) : (face == 1) ? (i == nx - 1) : (face == 2) ? (j == 0) : (j == ny - 1);
-                    if (!on) continue;
-                    double Mb[NQ], Mj[NQ];
-#pragma unroll
-                    for (int m = 0; m < NQ; ++m) Mb[m] = Mj[m] = 0.0;
-                    for (int dd = 0; dd < sd.nd; ++dd) {
-                        const double cb = coefS[dd * NFIELD + 6 + 2 * face], cj = coefS[dd * NFIELD + 7 + 2 * face];
-                        const double* Sp = S + (size_t)el * SEL + dd * NQ;
-#pragma unroll
-                        for (int m = 0; m < NQ; ++m) {
-                            Mb[m] = fma(cb, Sp[m], Mb[m]);
-                            Mj[m] = fma(cj, Sp[m], Mj[m]);
-                        }
-                    }
-#pragma unroll
-                    for (int t = 0; t < NP1; ++t) {
-                        int a, b, idx;
-                        if (face < 2) {
-                            a = (face == 0) ? 0 : P;
-                            b = t;
-                            idx = j;
-                        } else {
-                            b = (face == 2) ? 0 : P;
-                            a = t;
-                            idx = i;
-                        }
-                        const int kk = (fx ? P - a : a) + NP1 * (fy ? P - b : b);
-                        double vb = 0.0, vj = 0.0;
-                        if constexpr (P == 2) {
-#pragma unroll
-                            for (int m = 0; m < 9; ++m) {
-                                vb = fma(bckS[kk * 9 + m], Mb[m], vb);
-                                vj = fma(bckS[kk * 9 + m], Mj[m], vj);
-                            }
-                        } else {
-                            vb = Mb[kk];
-                            vj = Mj[kk];
-                        }
-                        const int bn = bnode2d(face, idx, t, nx, ny, NP1);
-                        slab[6 * nodes + bn] = vb;
-                        slab[6 * nodes + prm.nbnode + bn] = vj;
-                    }
-                }
-            }
+            if constexpr (!DEFER) phase_c(i0, cols, S);
+        }
+        if constexpr (DEFER) {  // the last chunk's direction sums
+            const int cl = prm.n_chunks - 1;
+            phase_c(cl * C, min(C, nx - cl * C), (cl & 1) ? Salt : S);
         }
 #ifdef SWEEP_TRACE
         if (tid == 0 && task < (1 << 18)) {
