@@ -497,8 +497,9 @@ __device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc,
 //      modal q^ (p=2) and sigma~ = sigma + 1/(c dt);
 //   B  every lane sweeps the chunk (branch-free: out-of-mesh rows/columns run on
 //      zeroed staging and are never written out);
-//   C  direction sums with the moment / boundary weights, back to nodal values,
-//      written to this stream's slab.
+//   C  direction sums with the moment / boundary weights, written to this stream's
+//      slab; with DEFER (default) chunk c-1's sums run between A and B of chunk c,
+//      while thread 0 waits for the strip below (S is double-buffered).
 // OPT bits (compile time): OPT_SIGMA appends sum_g sigma_g (phi, J) (NEXT-1), OPT_FIXUP
 // applies the zero-and-scale fixup to every element solve (NEXT-2).
 template <int P, int LOG2LG, int K, int OPT>
