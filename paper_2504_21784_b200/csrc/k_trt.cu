@@ -109,11 +109,20 @@ __device__ __forceinline__ void emission_sum_warp(double T, int G, const double*
                                                   double& d2E) {
     const double T2 = T * T, T3 = T2 * T, T4 = T3 * T, iT = 1.0 / T;
     double e = 0.0, de = 0.0, d2e = 0.0;
+    // top bound far in the Wien tail (x > 50: 1 - P < 1e-17, x P' < 1e-15): P = 1,
+    // h = q = 0 without evaluating it, which saves the round a lone bound G would take
+    // (G = 64: bounds 64 = 2 x 32 + 1); warp-uniform, every lane has the same T
+    const bool top_one = nu[G] * iT > 50.0;
+    const int last = top_one ? G - 1 : G;
     double carry_P = 0.0, carry_h = 0.0, carry_q = 0.0;  // bound 32k - 1 (lane 31 of the previous round)
-    for (int b0 = 0; b0 <= G; b0 += 32) {
+    double P = 0.0, h = 0.0, q = 0.0;
+    int b0 = 0;
+    for (; b0 <= last; b0 += 32) {
         const int bnd = b0 + lane;
-        double P = 0.0, h = 0.0, q = 0.0;
-        if (bnd <= G) {
+        P = 0.0;
+        h = 0.0;
+        q = 0.0;
+        if (bnd <= last) {
             const double x = nu[bnd] * iT;
             double dP, rem1;
             planck_P(x, P, dP, rem1);
@@ -127,7 +136,7 @@ __device__ __forceinline__ void emission_sum_warp(double T, int G, const double*
             hl = carry_h;
             ql = carry_q;
         }
-        if (bnd >= 1 && bnd <= G) {
+        if (bnd >= 1 && bnd <= last) {
             const double sg = sig[bnd - 1];
             const double dPg = P - Pl, dhg = h - hl, dqg = q - ql;
             e = fma(sg, T4 * dPg, e);
@@ -137,6 +146,20 @@ __device__ __forceinline__ void emission_sum_warp(double T, int G, const double*
         carry_P = __shfl_sync(0xffffffffu, P, 31);
         carry_h = __shfl_sync(0xffffffffu, h, 31);
         carry_q = __shfl_sync(0xffffffffu, q, 31);
+    }
+    if (top_one) {
+        // group G - 1 between bound G - 1 (held by lane last - (b0 - 32) of the last round)
+        // and bound G (P = 1, h = q = 0)
+        const int src = last - (b0 - 32);
+        const double Pl = __shfl_sync(0xffffffffu, P, src), hl = __shfl_sync(0xffffffffu, h, src),
+                     ql = __shfl_sync(0xffffffffu, q, src);
+        if (lane == 0) {
+            const double sg = sig[G - 1];
+            const double dPg = 1.0 - Pl, dhg = -hl, dqg = -ql;
+            e = fma(sg, T4 * dPg, e);
+            de = fma(sg, T3 * (4.0 * dPg - dhg), de);
+            d2e = fma(sg, T2 * (12.0 * dPg - 3.0 * dhg - dqg), d2e);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
