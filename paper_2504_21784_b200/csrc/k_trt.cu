@@ -67,33 +67,33 @@ __device__ __forceinline__ void planck_P(double x, double& P, double& dP, double
     }
 }
 
-// q[v][g] = sigma[e][g] B_g(T[v]) + Iprev[v][g] * inv_dt   (v = e*n + k).  One thread per
-// (node, group); each evaluates P at its upper bound only and takes the lower bound's value
-// from the neighbouring lane (the groups of a node are consecutive lanes); the first group
-// of a warp segment evaluates its lower bound itself.
+// q[v][g] = sigma[e][g] B_g(T[v]) + Iprev[v][g] * inv_dt   (v = e*n + k).  The (node,
+// bound) pairs are laid out flat, G + 1 slots per node; each warp evaluates P at 32
+// consecutive slots, overlapping the previous warp by one, so every lane evaluates P
+// exactly once and lanes 1..31 emit the group whose upper bound they hold (its lower
+// bound is the previous lane's slot).  (A thread per (node, group) with the first lane
+// of each warp evaluating its lower bound too made every warp pay two evaluations.)
 __global__ void trt_emission_kernel(const double* __restrict__ T, const double* __restrict__ sigma,
                                     const double* __restrict__ Iprev, const double* __restrict__ nu, int G, int n,
                                     size_t nodes, double inv_dt, double* __restrict__ q) {
-    const size_t total = nodes * G;
-    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t slots = nodes * (size_t)(G + 1);
     const int lane = threadIdx.x & 31;
-    for (size_t i0 = (size_t)blockIdx.x * blockDim.x; i0 < total; i0 += stride) {
-        const size_t i = i0 + threadIdx.x;
-        const bool on = i < total;
-        const size_t ii = on ? i : total - 1;
-        const size_t v = ii / G;
-        const int g = (int)(ii - v * G);
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t w = (((size_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); 31 * w + 1 < slots; w += warps) {
+        const size_t sl = 31 * w + lane;
+        const bool on = sl < slots;
+        const size_t ss = on ? sl : slots - 1;
+        const size_t v = ss / (size_t)(G + 1);
+        const int bnd = (int)(ss - v * (size_t)(G + 1));
         const double t = T[v];
-        const double it = 1.0 / t;
-        double Pr, d, d2;
-        planck_P(nu[g + 1] * it, Pr, d, d2);
-        double Pl = __shfl_up_sync(0xffffffffu, Pr, 1);
-        const double lo_from_left = __shfl_up_sync(0xffffffffu, (double)v, 1);
-        if (g == 0 || lane == 0 || lo_from_left != (double)v) planck_P(nu[g] * it, Pl, d, d2);
-        if (on) {
-            const size_t e = v / n;
+        double P, d, d2;
+        planck_P(nu[bnd] * (1.0 / t), P, d, d2);
+        const double Pl = __shfl_up_sync(0xffffffffu, P, 1);
+        if (on && lane >= 1 && bnd >= 1) {
+            const int g = bnd - 1;
+            const size_t ii = v * (size_t)G + g;
             const double t2 = t * t;
-            q[ii] = fma(sigma[e * G + g], t2 * t2 * (Pr - Pl), Iprev[ii] * inv_dt);
+            q[ii] = fma(sigma[(v / n) * G + g], t2 * t2 * (P - Pl), Iprev[ii] * inv_dt);
         }
     }
 }
