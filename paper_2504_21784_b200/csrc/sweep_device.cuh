@@ -893,14 +893,24 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #ifndef SWEEP_POLL_NS
 #define SWEEP_POLL_NS 0
 #endif
+                // (experiments: polling with ld.acquire, or a fence.acq_rel after the relaxed
+                // poll instead of the acquire load, were no faster: C4 1.02 / 1.08 ms)
+#if defined(SWEEP_POLL_ACQ)
+                while (ld_acquire(f) < c + 1) {
+#else
                 while (ld_relaxed_gpu(f) < c + 1) {
+#endif
                     if (SWEEP_POLL_NS > 0) __nanosleep(SWEEP_POLL_NS);
                     if (clock64() - t_start > (1LL << 34)) {
                         atomicOr(prm.err, 4);
                         break;
                     }
                 }
+#if defined(SWEEP_POLL_FENCE)
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#elif !defined(SWEEP_POLL_ACQ)
                 (void)ld_acquire(f);
+#endif
 #ifdef SWEEP_TRACE
                 t_waited += gtimer() - w0;
 #endif
