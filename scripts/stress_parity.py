@@ -45,5 +45,8 @@ for i in range(n):
         print(f"note dim={dim} p={p} nx={nx} ny={ny} G={G} nd={nd} opts={opts} err={m:.2e} field={worst_k}", flush=True)
     if not ok:
         fails += 1
-        print(f"FAIL dim={dim} p={p} nx={nx} ny={ny} G={G} nd={nd} opts={opts} err={m:.2e}", flush=True)
+        print(f"FAIL i={i} dim={dim} p={p} nx={nx} ny={ny} G={G} nd={nd} opts={opts} err={m:.2e}", flush=True)
+        if np.isfinite(m):
+            print("     ", {k: (f"{v[0]:.2e}", v[1]) for k, v in e.items()}, flush=True)
+            print("      omega", np.round(prob.omega, 4).tolist(), "w", np.round(prob.w, 4).tolist(), flush=True)
 print(f"{ran} of {n} cases run, {fails} failures, worst relative error {worst:.2e}, {time.time() - t0:.0f} s", flush=True)
