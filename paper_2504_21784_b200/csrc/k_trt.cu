@@ -177,7 +177,10 @@ __device__ __forceinline__ void emission_sum_warp(double T, int G, const double*
 // (dT^2, T^2) for the convergence test (summed in a fixed order afterwards).  One warp
 // per node: nodes converge after different numbers of steps, and a thread per node
 // made every warp wait for its slowest node.
-__global__ void __launch_bounds__(256) trt_update_kernel(const double* __restrict__ Tk, double* __restrict__ T,
+#ifndef SWEEP_TRT_MINB
+#define SWEEP_TRT_MINB 3  // 72 registers, 3 blocks of 256 per SM, grid 3 x 148: C5 TRT 23.9 -> 23.4 ms
+#endif
+__global__ void __launch_bounds__(256, SWEEP_TRT_MINB) trt_update_kernel(const double* __restrict__ Tk, double* __restrict__ T,
                                                          const double* __restrict__ sphi, const double* __restrict__ sigma,
                                                          const double* __restrict__ nu, int G, int n, size_t nodes,
                                                          double cv_dt, double* __restrict__ partial, int* err) {
@@ -273,7 +276,10 @@ __global__ void trt_norm_kernel(const double* __restrict__ partial, int nblocks,
     }
 }
 
-int trt_blocks() { return 148 * 4; }
+#ifndef SWEEP_TRT_BPS
+#define SWEEP_TRT_BPS 3
+#endif
+int trt_blocks() { return 148 * SWEEP_TRT_BPS; }
 
 int launch_trt_emission(const double* T, const double* sigma, const double* Iprev, const double* nu, int G, int n,
                         size_t nodes, double inv_dt, double* q, void* stream) {
