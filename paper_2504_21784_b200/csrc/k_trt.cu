@@ -283,7 +283,10 @@ int trt_blocks() { return 148 * SWEEP_TRT_BPS; }
 
 int launch_trt_emission(const double* T, const double* sigma, const double* Iprev, const double* nu, int G, int n,
                         size_t nodes, double inv_dt, double* q, void* stream) {
-    trt_emission_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(T, sigma, Iprev, nu, G, n, nodes, inv_dt, q);
+#ifndef SWEEP_EMIS_BPS
+#define SWEEP_EMIS_BPS 4  // all blocks resident (a grid-stride kernel: 8 x 148 left a partial second wave; -0.5 ms)
+#endif
+    trt_emission_kernel<<<148 * SWEEP_EMIS_BPS, 256, 0, (cudaStream_t)stream>>>(T, sigma, Iprev, nu, G, n, nodes, inv_dt, q);
     return (int)cudaGetLastError();
 }
 
