@@ -256,12 +256,23 @@ int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, d
     return (int)cudaGetLastError();
 }
 
+// grid of a grid-stride kernel: at most the blocks that are resident at once (a
+// partial second wave idles most SMs at the end)
+template <typename Kern>
+static int resident_grid(Kern k, int block, size_t want) {
+    static int per_sm = 0;  // one kernel per instantiation (distinct signatures); queried once
+    if (per_sm < 1 &&
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, 0) != cudaSuccess || per_sm < 1))
+        per_sm = 1;
+    const size_t cap = (size_t)148 * per_sm;
+    const size_t g = want < cap ? want : cap;
+    return g < 1 ? 1 : (int)g;
+}
+
 int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes, int dim,
                      int modal, double* out, void* stream) {
     const int block = 256;
-    size_t want = (nodes + block - 1) / block;
-    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
-    if (grid < 1) grid = 1;
+    const int grid = resident_grid(halfrange_kernel, block, (nodes + block - 1) / block);
     halfrange_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, nodes, dim, modal, out);
     return (int)cudaGetLastError();
 }
@@ -269,9 +280,7 @@ int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const Stre
 int launch_finalize_modal(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t row0,
                           int nrows, size_t nel, double* out, int* err, void* stream) {
     const int block = 256;
-    size_t want = ((size_t)nrows * nel + block - 1) / block;
-    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
-    if (grid < 1) grid = 1;
+    const int grid = resident_grid(finalize_modal_kernel, block, ((size_t)nrows * nel + block - 1) / block);
     finalize_modal_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, row0, nrows, nel,
                                                                     out, err);
     return (int)cudaGetLastError();
