@@ -193,6 +193,73 @@ def run_reference(args, prob) -> dict:
             "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def front_occupancy(prob, n_dir_quad: int, G: int, capacity: int) -> float:
+    """sum_k min(active_k, capacity) / (#fronts x capacity) for the anti-diagonal
+    fronts k of one quadrant sweep, all quadrants concurrent; a work item is one
+    (element, direction, group) solve, capacity = resident lanes x groups per lane."""
+    if prob.dim == 1:
+        fronts = np.ones(prob.nx)
+        nq = 2
+    else:
+        k = np.arange(prob.nx + prob.ny - 1)
+        fronts = np.minimum(np.minimum(k + 1, prob.nx), np.minimum(prob.ny, prob.nx + prob.ny - 1 - k))
+        nq = 4
+    active = fronts * n_dir_quad * G * nq
+    return float(np.minimum(active, capacity).sum() / (fronts.size * capacity))
+
+
+def graph_replay_ms(sw, run, stream, reps: int = 20):
+    """Time of one step replayed from a CUDA graph captured around `run` (the same kernels
+    and memsets as the eager step, without the host enqueue cost)."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        run()   # warm on the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.replay()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def parity_sample(prob, shard, sw, dev):
+    """Oracle-vs-GPU parity on sampled outputs of the bench's own handle (same launch
+    configuration as the timed steps, full mesh): every group but the shard's first gets a
+    zero source and zero inflow, so the gray output is that one group's contribution; the
+    oracle computes group 0 alone.  Returns the per-field errors (tests/parity.py metric)."""
+    import torch
+    import oracle
+    from tests.parity import field_errors, field_ok
+    oracle.build()
+    q0 = np.zeros_like(shard.q)
+    q0[..., 0] = shard.q[..., 0]
+    f0 = np.zeros_like(shard.inflow)
+    f0[:, 0] = shard.inflow[:, 0]
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    sw.sweep_run(t(shard.sigma), prob.inv_c_dt, t(q0), t(f0))
+    got = sw.closures_get().cpu().numpy()
+    one = shard.group_slice(0, 1)
+    t0 = time.perf_counter()
+    ref = oracle.sweep(one)
+    errs = field_errors(got[:ref.size], ref, prob.dim, prob.nx, prob.ny, prob.p)
+    return {"sample": f"group 0 of {shard.G} (others zero), full mesh, all {prob.n_dir} directions, "
+                      f"bench launch configuration",
+            "max_error": max(e for e, _ in errs.values()),
+            "all_pass": all(field_ok(v) for v in errs.values()),
+            "fields": {k: [float(e), kind] for k, (e, kind) in errs.items()},
+            "oracle_s": time.perf_counter() - t0}
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -203,7 +270,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--lib", default=None, help="another build of libsweep.so (experiment builds only, "
+                                                  "scripts/build_variants.py)")
     ap.add_argument("--opts", default="", help="comma list of NEXT-row options: sigma (sigma-weighted moments), "
                                                  "fixup (zero-and-scale negative flux fixup), halfrange "
                                                  "(half-range moments of the consistent method), trt (one "
@@ -233,6 +303,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
+    if args.lib:
+        pk.load_library(args.lib)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
 
@@ -269,13 +341,21 @@ def main():
         Tout = torch.empty_like(Tk)
         trt_dt = 1.0 / prob.inv_c_dt
 
-    def step():
-        if flush.numel():
-            flush.zero_()
+    def work():
         if "trt" in opts:
             sw.trt_step(sig, fl, Tk, Ip, nu, cv=1.0, dt=trt_dt, eps=0.0, max_iter=1, T=Tout)
         else:
             sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+
+    def step(evs=None):
+        # the L2 flush (small configs) runs before the step's own events
+        if flush.numel():
+            flush.zero_()
+        if evs:
+            evs[0].record(stream)
+        work()
+        if evs:
+            evs[1].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -291,9 +371,11 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
     ev0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for k in range(args.steps):
+        step(step_evs[k])
     ev1.record(stream)
     torch.cuda.synchronize()
     if ws > 1:
@@ -302,13 +384,28 @@ def main():
     total_ms = ev0.elapsed_time(ev1)
     kt = sw.kernel_times(args.steps)
     sw.timing(False)
-    step_ms = float(kt.sum(axis=1).mean()) if flush.numel() else total_ms / args.steps
+    # with the flush, a step is timed from its own events (emission, update and the host
+    # sync of the TRT option included); without it, over the whole timed region
+    step_ms = (float(np.mean([a.elapsed_time(b) for a, b in step_evs])) if flush.numel()
+               else total_ms / args.steps)
     t = torch.tensor([step_ms, float(kt[:, 0].mean())], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, sweep_ms = float(t[0]), float(t[1])
     sw.closures_get(out)
-    launches_per_step = sw.stats()["launches"] + (3 if "trt" in opts else 0)  # + emission, update, norm
+    stats = sw.stats()
+    launches_per_step = stats["launches"] + (3 if "trt" in opts else 0)  # + emission, update, norm
+    # latency floors (C1-C3 are reported against them): an empty kernel launch,
+    # and the same step replayed from a CUDA graph
+    floors = None
+    if "trt" not in opts:
+        try:
+            floors = {"empty_launch_us": pk.launch_floor(local),
+                      "graph_replay_ms": graph_replay_ms(sw, lambda: sw.sweep_run(sig, prob.inv_c_dt, q, fl), stream),
+                      "launches_per_step": launches_per_step}
+            floors["step_floor_ms"] = floors["empty_launch_us"] * launches_per_step * 1e-3
+        except Exception as ex:  # noqa: BLE001
+            floors = {"error": str(ex)[:200]}
 
     # ---- end to end through the host API (pinned buffers), same metric
     e2e = None
@@ -333,6 +430,10 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": prob.unknowns / (float(te[0]) * 1e-3), "unit": "unknowns/s",
                "ms_per_step": float(te[0]), "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": 8 * sw.out_size}
+
+    parity = None
+    if ws == 1 and not args.no_parity and not opts:
+        parity = parity_sample(prob, shard, sw, dev)
 
     if rank == 0:
         nd = distinct_dirs(prob)
@@ -381,6 +482,10 @@ def main():
                                  "peak_gbs_measured": peaks.get("hbm_gbs"),
                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (b.copy_(a), read+write)"}},
             "gpu_launches": int(launches_per_step * args.steps),
+            "floors": floors,
+            "front_occupancy": front_occupancy(prob, nd // (4 if prob.dim == 2 else 2), shard.G,
+                                               stats["ctas"] * stats["block"] * stats["groups_per_lane"]),
+            "parity": parity,
             "clocks": clk,
             "step_breakdown_ms": {"sweep": float(kt[:, 0].mean()), "finalize": float(kt[:, 1].mean()),
                                   "allreduce": float(kt[:, 2].mean())},
@@ -398,6 +503,13 @@ def main():
                                    "kind": "oracle",
                                    "sample": f"{prob.name} mesh, all {prob.n_dir} directions, 1 of {prob.G} groups "
                                              f"({sample.unknowns} unknowns, {dt:.1f} s)"}
+            if prob.dim == 1 or prob.n_el * prob.n * prob.n_dir <= 2 ** 25:
+                # single-core oracle (C1-C4), same sample
+                t0 = time.perf_counter()
+                oracle.sweep(sample, nthreads=1)
+                d1 = time.perf_counter() - t0
+                rec["cpu_baseline"]["single_core"] = {"value": sample.unknowns / d1, "unit": "unknowns/s",
+                                                      "cores": 1, "seconds": d1}
         print(json.dumps(rec), flush=True)
     sw.close()
     if ws > 1:

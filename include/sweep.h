@@ -88,6 +88,9 @@ enum {
                                     sum_k W_k psi_k (W_k the lumped GLL mass); a non-positive integral
                                     zeroes the element.  The downwind elements see the fixed values.
                                     Nonlinear: no longer the solution of one linear system. */
+#define SWEEP_FORCE_COMM 32u     /* with nranks = 1 and a nccl_id: still build a 1-rank NCCL communicator
+                                    and end every sweep_run with the (trivial) all-reduce, so the
+                                    collective's plumbing can be exercised on a single GPU */
 
 typedef struct sweep_handle sweep_handle;   /* opaque, owned by the library */
 
@@ -105,7 +108,8 @@ typedef struct {
     int device;              /* CUDA device ordinal */
     int nranks, rank;        /* nranks = 1: no collective; > 1: NCCL all-reduce of the gray output */
     const void *nccl_id;     /* 128-byte ncclUniqueId created by rank 0 and broadcast (nranks > 1), else NULL */
-    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC | SWEEP_SIGMA_MOMENTS | SWEEP_FIXUP | SWEEP_HALF_RANGE */
+    unsigned flags;          /* SWEEP_FOLD_Z | SWEEP_DETERMINISTIC | SWEEP_SIGMA_MOMENTS | SWEEP_FIXUP | SWEEP_HALF_RANGE
+                                | SWEEP_FORCE_COMM */
 } sweep_desc;
 
 /* Validate the description, fold/sort directions into sweep quadrants,
@@ -149,8 +153,13 @@ int sweep_run_host(sweep_handle *h, const double *h_sigma, double inv_c_dt, cons
  *             T <- root of C_v (T - T^k)/dt + sum_g sigma_g B_g(T) = sum_g sigma_g phi_g
  *                  at every node (pointwise nonlinear elimination, PAPER.md:588-596;
  *                  bracketed Newton to 1e-15 relative)
- *   } until ||T_new - T||_2 <= eps ||T_new||_2 (eq:relative_tol; paper: eps = 1e-4 for this
- *   scheme) or max_iter iterations.
+ *   } until the paper's relative stopping criterion (eq:relative_tol)
+ *       ||u^l - u^{l-1}||_2 < eps ||u^1 - u^0||_2,   u = [T, E]   (paper: eps = 1e-4 for this
+ *   scheme), checked after every iteration l >= 2 (after l = 1 only when
+ *   u^1 = u^0 exactly), or max_iter iterations.  u^0 is the initial guess on entry:
+ *   T^0 = T^k and E^0 = sum_g I^k_g (c = 1, sum_d w_d = 1: the energy density of the
+ *   isotropic I^k); E^l = phi of the l-th sweep (c E = phi); the norm
+ *   is the 2-norm of the nodal coefficient vectors of T and E together (reading R24).
  * B_g(T) = T^4 [P(nu_{g+1}/T) - P(nu_g/T)], P the normalised Planck integral (a = c = 1).
  * Requires a handle set up with SWEEP_SIGMA_MOMENTS and nranks = 1.
  *   d_sigma [N_el][G], d_inflow [N_bnode][G]  as for sweep_run (sigma at T^k: explicit)
@@ -166,15 +175,23 @@ typedef struct {
     double dt;          /* time step > 0 */
     double eps;         /* relative tolerance of the outer iteration; <= 0: run max_iter */
     int max_iter;       /* >= 1 */
+    double *ratios;     /* HOST [max_iter] or NULL: receives ||u^l - u^{l-1}||_2 / ||u^1 - u^0||_2
+                           for l = 1 .. *iterations (0 when u^1 = u^0) */
 } trt_params;
 
 int trt_step(sweep_handle *h, const double *d_sigma, const double *d_inflow, const double *d_Tk,
              const double *d_Iprev, const trt_params *prm, double *d_T, int *iterations, void *cuda_stream);
 
-/* Statistics of the last sweep_run: number of kernels launched (out[0]),
- * distinct directions swept (out[1], after folding), work streams (out[2]),
- * persistent CTAs (out[3]). */
-int sweep_stats(const sweep_handle *h, long long out[4]);
+/* Statistics of the handle and its last sweep_run: out[0] kernels launched by the last
+ * sweep_run, out[1] distinct directions swept (after folding), out[2] work streams,
+ * out[3] CTAs of the sweep kernel, out[4] threads per CTA, out[5] groups per lane,
+ * out[6] lanes per direction, out[7] SMs of the device. */
+int sweep_stats(const sweep_handle *h, long long out[8]);
+
+/* Launch-latency floor of the device: back-to-back launches of an empty kernel on one
+ * stream, device time per launch in microseconds (the floor the latency-bound configs
+ * C1-C3 are reported against). */
+int sweep_launch_floor(int device, int reps, double *us_per_launch);
 
 /* Per-run kernel timing (CUDA events recorded on the run's stream around the
  * sweep kernel, the finalize kernel and the all-reduce).  enable != 0 clears

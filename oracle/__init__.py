@@ -58,7 +58,7 @@ def _load():
         lib.oracle_planck_groups.restype = None
         lib.oracle_t_eliminate.argtypes = [d, d, i, dp, dp, d]
         lib.oracle_t_eliminate.restype = d
-        lib.oracle_trt_step.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, dp, dp, dp, dp, d, d, d, i, dp, i]
+        lib.oracle_trt_step.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, dp, dp, dp, dp, d, d, d, i, dp, dp, i]
         lib.oracle_trt_step.restype = i
         lib.oracle_sweep_psi.argtypes = [i, i, i, d, d, i, i, dp, dp, i, dp, d, dp, dp, i, i, dp, i]
         lib.oracle_sweep_psi.restype = i
@@ -128,18 +128,24 @@ def t_eliminate(Tk: float, sphi: float, sigma_g, nu, cv_dt: float) -> float:
 
 
 def trt_step(prob, Tk, Iprev, nu, cv: float, dt: float, eps: float = 1e-4, max_iter: int = 50,
-             nthreads: int = 0):
+             nthreads: int = 0, return_ratios: bool = False):
     """One unaccelerated backward-Euler TRT step (NEXT-4).  prob supplies mesh, quadrature,
-    sigma [N_el][G] and inflow; Tk [N_el][n], Iprev [N_el][n][G].  Returns (T, iterations)."""
+    sigma [N_el][G] and inflow; Tk [N_el][n], Iprev [N_el][n][G].  Stops on eq:relative_tol
+    (PAPER.md:657-660): ||u^l - u^(l-1)||_2 < eps ||u^1 - u^0||_2 with u = [T, E], E^0 =
+    sum_g I^k_g, E^l = phi of the l-th sweep.  Returns (T, iterations) or, with
+    return_ratios, (T, iterations, ratios[l-1] = ||u^l - u^(l-1)|| / ||u^1 - u^0||)."""
     lib = _load()
     om, w, s, fl = _c(prob.omega), _c(prob.w), _c(prob.sigma), _c(prob.inflow)
     Tk, Ip, nu = _c(Tk), _c(Iprev), _c(nu)
     T = np.zeros_like(Tk)
+    ratios = np.zeros(max(1, int(max_iter)))
     rc = lib.oracle_trt_step(prob.dim, prob.nx, prob.ny, prob.lx, prob.ly, prob.p, om.shape[0], _ptr(om), _ptr(w),
                              s.shape[1], _ptr(s), _ptr(fl), _ptr(Tk), _ptr(Ip), _ptr(nu), float(cv), float(dt),
-                             float(eps), int(max_iter), _ptr(T), int(nthreads))
+                             float(eps), int(max_iter), _ptr(T), _ptr(ratios), int(nthreads))
     if rc < 0:
         raise RuntimeError(f"oracle_trt_step failed rc={rc}")
+    if return_ratios:
+        return T, rc, ratios[:rc].copy()
     return T, rc
 
 

@@ -42,7 +42,13 @@
  * from the current temperature (eq:smm_be_transport; c = 1); sweep;
  * pointwise nonlinear elimination of T from the energy balance
  *     C_v (T - T^k)/dt = sum_g sigma_g (phi_g - B_g(T))   (eq:smm_be_meb)
- * } until ||T^{l+1} - T^l||_2 <= eps ||T^{l+1}||_2 (eq:relative_tol).
+ * } until the paper's relative stopping criterion (eq:relative_tol,
+ * PAPER.md:657-660; eps = 1e-4 for the unaccelerated scheme)
+ *     ||u^{l+1} - u^l||_2 < eps ||u^1 - u^0||_2,   u = [T, E]
+ * with u^0 the initial guess on entry (T^0 = T^k, E^0 = E^k = sum_g I^k_g: c = 1 and
+ * sum_d w_d = 1, so the energy density of the isotropic I^k is its group sum) and
+ * E^l = phi^l = sum_g sum_d w_d psi (c E = phi) of the l-th sweep;
+ * the 2-norm is over the nodal coefficient vectors of T and E (reading R24).
  * B_g(T) = T^4 [P(nu_{g+1}/T) - P(nu_g/T)], P(x) = (15/pi^4) int_0^x t^3/(e^t-1) dt
  * (eq:planck PAPER.md:106-125, a = c = 1) evaluated here by composite Gauss-Legendre
  * quadrature of the integrand (no series), and T found by bisection (no Newton).
@@ -625,12 +631,16 @@ double oracle_t_eliminate(double Tk, double sphi, int G, const double *sig, cons
 
 /* One unaccelerated backward-Euler step.  Tk, T [N_el][n] nodal; Iprev [N_el][n][G]
  * isotropic previous intensity; sigma [N_el][G]; inflow [N_bnode][G]; nu [G+1].
- * c = 1: 1/(c dt) = 1/dt.  Runs until the relative 2-norm change is <= eps (eps > 0)
- * or max_iter iterations; returns the iteration count, or < 0 on failure. */
+ * c = 1: 1/(c dt) = 1/dt.  Iteration l = 1, 2, ...: u^l = [T^l, E^l]; stops after the
+ * first iteration l >= 2 with ||u^l - u^{l-1}||_2 < eps ||u^1 - u^0||_2 (eq:relative_tol,
+ * PAPER.md:657-660), or after iteration 1 when ||u^1 - u^0||_2 = 0 (u^0 is already the
+ * fixed point), or after max_iter iterations; eps <= 0 runs max_iter.  ratio (may be
+ * NULL) receives ||u^l - u^{l-1}||_2 / ||u^1 - u^0||_2 for l = 1..iterations.
+ * Returns the iteration count, or < 0 on failure. */
 int oracle_trt_step(int dim, int nx, int ny, double lx, double ly, int p, int ndir, const double *omega,
                     const double *w, int G, const double *sigma, const double *inflow, const double *Tk,
                     const double *Iprev, const double *nu, double cv, double dt, double eps, int max_iter,
-                    double *T, int nthreads) {
+                    double *T, double *ratio, int nthreads) {
     prob P;
     int rc = setup(&P, dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, 1.0 / dt, Iprev, inflow);
     if (rc) return rc;
@@ -641,9 +651,16 @@ int oracle_trt_step(int dim, int nx, int ny, double lx, double ly, int p, int nd
     double *q = (double *)malloc(sizeof(double) * nodes * G);
     double *out = (double *)malloc(sizeof(double) * nout);
     double *Tn = (double *)malloc(sizeof(double) * nodes);
+    double *E = (double *)malloc(sizeof(double) * nodes);
     double *Bg = (double *)malloc(sizeof(double) * G);
-    if (!q || !out || !Tn || !Bg) { free(q); free(out); free(Tn); free(Bg); return -3; }
-    for (size_t v = 0; v < nodes; ++v) T[v] = Tk[v];
+    if (!q || !out || !Tn || !E || !Bg) { free(q); free(out); free(Tn); free(E); free(Bg); return -3; }
+    for (size_t v = 0; v < nodes; ++v) {
+        T[v] = Tk[v];
+        double e = 0.0;                 /* E^0 = sum_g I^k_g (isotropic, sum_d w_d = 1) */
+        for (int g = 0; g < G; ++g) e += Iprev[v * G + g];
+        E[v] = e;
+    }
+    double first = 0.0;                 /* ||u^1 - u^0||_2 */
     int it = 0;
     for (it = 1; it <= max_iter; ++it) {
         for (size_t v = 0; v < nodes; ++v) {
@@ -653,17 +670,23 @@ int oracle_trt_step(int dim, int nx, int ny, double lx, double ly, int p, int nd
         }
         rc = oracle_sweep2(dim, nx, ny, lx, ly, p, ndir, omega, w, G, sigma, 1.0 / dt, q, inflow, out, nthreads, 1);
         if (rc) break;
-        double dn = 0.0, tn = 0.0;
+        double du = 0.0;                /* ||u^it - u^(it-1)||_2^2 over T and E = phi */
         for (size_t v = 0; v < nodes; ++v) {
             const size_t e = v / P.n;
             Tn[v] = oracle_t_eliminate(Tk[v], out[off_sig + v], G, sigma + e * G, nu, cv / dt);
-            dn += (Tn[v] - T[v]) * (Tn[v] - T[v]);
-            tn += Tn[v] * Tn[v];
+            du += (Tn[v] - T[v]) * (Tn[v] - T[v]);
+            du += (out[v] - E[v]) * (out[v] - E[v]);
         }
-        for (size_t v = 0; v < nodes; ++v) T[v] = Tn[v];
-        if (eps > 0.0 && sqrt(dn) <= eps * sqrt(tn)) break;
+        for (size_t v = 0; v < nodes; ++v) {
+            T[v] = Tn[v];
+            E[v] = out[v];
+        }
+        const double dn = sqrt(du);
+        if (it == 1) first = dn;
+        if (ratio) ratio[it - 1] = (first > 0.0) ? dn / first : 0.0;
+        if (eps > 0.0 && (first == 0.0 || (it >= 2 && dn < eps * first))) break;
     }
     if (it > max_iter) it = max_iter;
-    free(q); free(out); free(Tn); free(Bg);
+    free(q); free(out); free(Tn); free(E); free(Bg);
     return rc ? rc : it;
 }

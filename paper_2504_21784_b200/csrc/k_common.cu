@@ -81,76 +81,48 @@ __global__ void finalize_modal_kernel(const double* __restrict__ slabs, int n_sl
 // out rows (2-D): Fx+[x,y], Px+[xx,xy,yy], Fy+[x,y], Py+[xx,xy,yy]; (1-D): F+, P+.
 // modal != 0 (2-D p = 2): the slab rows hold modal values (see finalize_modal_kernel).
 __global__ void halfrange_kernel(const double* __restrict__ slabs, int n_slabs, size_t stride,
-                                 const StreamDesc* __restrict__ streams, size_t nodes, int dim, int modal,
+                                 const StreamDesc* __restrict__ streams, size_t nodes, size_t hr_off, int dim, int modal,
                                  double* __restrict__ out) {
-    const double third = 1.0 / 3.0;
     __shared__ double bck[81];  // (see finalize_modal_kernel)
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < 81; ++i) bck[i] = cM.bck[i / 9][i % 9];
     }
     __syncthreads();
+    // slab rows per stream: J_x, J_y at 1, 2; T_xy at 4; the untraced P_xx, P_yy the sweep
+    // wrote at hr_off, hr_off + 1 (rows of `nodes` doubles)
     for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += (size_t)gridDim.x * blockDim.x) {
-        if (modal) {
+        if (dim == 2) {
+            double a[10];
+#pragma unroll
+            for (int m = 0; m < 10; ++m) a[m] = 0.0;
             const size_t e9 = (v / 9) * 9;
             const int k = (int)(v - e9);
-            double a[10];
-#pragma unroll
-            for (int m = 0; m < 10; ++m) a[m] = 0.0;
-            for (int s = 0; s < n_slabs; ++s) {
-                const double* sl = slabs + (size_t)s * stride + e9;
-                const int q = streams[s].quadrant;
-                const int kk = sweep_node_of(k, q);
-                double f6[6];
-#pragma unroll
-                for (int f = 0; f < 6; ++f) {
-                    double x = 0.0;
-#pragma unroll
-                    for (int j = 0; j < 9; ++j) x = fma(bck[kk * 9 + j], sl[(size_t)f * nodes + j], x);
-                    f6[f] = x;
-                }
-                const double jx = f6[1], jy = f6[2], pxx = f6[3] + third * f6[0], pxy = f6[4],
-                             pyy = f6[5] + third * f6[0];
-                if (!(q & 1)) {
-                    a[0] += jx;
-                    a[1] += jy;
-                    a[2] += pxx;
-                    a[3] += pxy;
-                    a[4] += pyy;
-                }
-                if (!(q & 2)) {
-                    a[5] += jx;
-                    a[6] += jy;
-                    a[7] += pxx;
-                    a[8] += pxy;
-                    a[9] += pyy;
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < 10; ++m) out[(size_t)m * nodes + v] = a[m];
-        } else if (dim == 2) {
-            double a[10];
-#pragma unroll
-            for (int m = 0; m < 10; ++m) a[m] = 0.0;
             for (int s = 0; s < n_slabs; ++s) {
                 const double* sl = slabs + (size_t)s * stride;
                 const int q = streams[s].quadrant;
-                const double ph = sl[v], jx = sl[nodes + v], jy = sl[2 * nodes + v];
-                const double pxx = sl[3 * nodes + v] + third * ph, pxy = sl[4 * nodes + v],
-                             pyy = sl[5 * nodes + v] + third * ph;
+                const size_t rows[5] = {nodes, 2 * nodes, hr_off, 4 * nodes, hr_off + nodes};  // Jx Jy Pxx Pxy Pyy
+                double f5[5];
+                if (modal) {
+                    const int kk = sweep_node_of(k, q);
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) {
+                        double x = 0.0;
+#pragma unroll
+                        for (int j = 0; j < 9; ++j) x = fma(bck[kk * 9 + j], sl[rows[f] + e9 + j], x);
+                        f5[f] = x;
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) f5[f] = sl[rows[f] + v];
+                }
                 if (!(q & 1)) {
-                    a[0] += jx;
-                    a[1] += jy;
-                    a[2] += pxx;
-                    a[3] += pxy;
-                    a[4] += pyy;
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) a[f] += f5[f];
                 }
                 if (!(q & 2)) {
-                    a[5] += jx;
-                    a[6] += jy;
-                    a[7] += pxx;
-                    a[8] += pxy;
-                    a[9] += pyy;
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) a[5 + f] += f5[f];
                 }
             }
 #pragma unroll
@@ -161,7 +133,7 @@ __global__ void halfrange_kernel(const double* __restrict__ slabs, int n_slabs, 
                 if (streams[s].quadrant & 1) continue;
                 const double* sl = slabs + (size_t)s * stride;
                 f += sl[nodes + v];
-                pp += sl[2 * nodes + v] + third * sl[v];
+                pp += sl[hr_off + v];
             }
             out[v] = f;
             out[nodes + v] = pp;
@@ -187,7 +159,11 @@ static const void* pick1d(int log2gb, int opt) {
         case 0: return pick1d_lg<P, 0>(log2gb);
         case 1: return pick1d_lg<P, 1>(log2gb);
         case 2: return pick1d_lg<P, 2>(log2gb);
-        default: return pick1d_lg<P, 3>(log2gb);
+        case 3: return pick1d_lg<P, 3>(log2gb);
+        case 4: return pick1d_lg<P, 4>(log2gb);
+        case 5: return pick1d_lg<P, 5>(log2gb);
+        case 6: return pick1d_lg<P, 6>(log2gb);
+        default: return pick1d_lg<P, 7>(log2gb);
     }
 }
 
@@ -215,17 +191,28 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
     // sigma moments: S2; otherwise (DEFER, not for one group per direction) a second S buffer
     const bool defer = SWEEP_DEFER_C && !(k == 1 && gbk == 1);
     const int s2 = ((opt & OPT_SIGMA) || defer) ? CT * (dset * NQ + 1) : 0;
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 14 + k * (p + 1) * NL + 81 + s2) *
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + dset * 16 + k * (p + 1) * NL + 81 + s2) *
            (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
 int sweep2d_cols_per_chunk(int p, int k, int opt) { return cols_per_chunk(p, k, opt); }
 
+// The dynamic shared-memory cap is one value per kernel for the whole process, so it is
+// always raised to the device's opt-in maximum (never to one handle's size: a smaller
+// value set by a later handle would make an earlier handle's larger launch fail).
+static int raise_smem_cap(const void* f) {
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    return (int)e;
+}
+
 int sweep2d_occupancy(int p, int log2lg, int k, int opt, int block, size_t smem, int* blocks_per_sm) {
     const void* f = pick2d(p, log2lg, k, opt);
     if (!f) return (int)cudaErrorInvalidDeviceFunction;
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
+    int e = raise_smem_cap(f);
+    if (e) return e;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
 }
 
@@ -240,47 +227,55 @@ int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, 
 int launch_sweep1d(int p, int log2gb, int opt, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream) {
     const void* f = (p == 2) ? pick1d<2>(log2gb, opt) : pick1d<1>(log2gb, opt);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
+        const int e = raise_smem_cap(f);
+        if (e) return e;
     }
     void* args[] = {(void*)&prm};
     return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
 }
 
-int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, void* stream) {
+// grid of a grid-stride kernel: at most the blocks that are resident at once (a
+// partial second wave idles most SMs at the end); cap = SMs x resident blocks per SM,
+// computed per handle at setup (reduce_caps)
+static int capped_grid(size_t want, int cap) {
+    const size_t g = want < (size_t)cap ? want : (size_t)cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+int reduce_caps(int n_sm, ReduceCaps* caps) {
     const int block = 256;
-    size_t want = (n + block - 1) / block;
-    int grid = (int)(want < 148 * 8 ? want : 148 * 8);
-    if (grid < 1) grid = 1;
+    int a = 0, b = 0, c = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, finalize_kernel, block, 0);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finalize_modal_kernel, block, 0);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, halfrange_kernel, block, 0);
+    if (e != cudaSuccess) return (int)e;
+    caps->finalize = n_sm * (a > 0 ? a : 1);
+    caps->finalize_modal = n_sm * (b > 0 ? b : 1);
+    caps->halfrange = n_sm * (c > 0 ? c : 1);
+    return 0;
+}
+
+int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, int cap,
+                    void* stream) {
+    const int block = 256;
+    const int grid = capped_grid((n + block - 1) / block, cap);
     finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, n, out, err);
     return (int)cudaGetLastError();
 }
 
-// grid of a grid-stride kernel: at most the blocks that are resident at once (a
-// partial second wave idles most SMs at the end)
-template <typename Kern>
-static int resident_grid(Kern k, int block, size_t want) {
-    static int per_sm = 0;  // one kernel per instantiation (distinct signatures); queried once
-    if (per_sm < 1 &&
-        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, 0) != cudaSuccess || per_sm < 1))
-        per_sm = 1;
-    const size_t cap = (size_t)148 * per_sm;
-    const size_t g = want < cap ? want : cap;
-    return g < 1 ? 1 : (int)g;
-}
-
-int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes, int dim,
-                     int modal, double* out, void* stream) {
+int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes,
+                     size_t hr_off, int dim, int modal, double* out, int cap, void* stream) {
     const int block = 256;
-    const int grid = resident_grid(halfrange_kernel, block, (nodes + block - 1) / block);
-    halfrange_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, nodes, dim, modal, out);
+    const int grid = capped_grid((nodes + block - 1) / block, cap);
+    halfrange_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, nodes, hr_off, dim, modal,
+                                                               out);
     return (int)cudaGetLastError();
 }
 
 int launch_finalize_modal(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t row0,
-                          int nrows, size_t nel, double* out, int* err, void* stream) {
+                          int nrows, size_t nel, double* out, int* err, int cap, void* stream) {
     const int block = 256;
-    const int grid = resident_grid(finalize_modal_kernel, block, ((size_t)nrows * nel + block - 1) / block);
+    const int grid = capped_grid(((size_t)nrows * nel + block - 1) / block, cap);
     finalize_modal_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, streams, row0, nrows, nel,
                                                                     out, err);
     return (int)cudaGetLastError();
@@ -308,6 +303,33 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters
     }
     const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
     if (r == 1.2345) sink[threadIdx.x] = r;  // keep the chains alive
+}
+
+// empty-kernel launch floor: reps back-to-back launches of an empty kernel on one stream,
+// timed with events on that stream (device-side time per launch, host enqueue overlapped)
+__global__ void empty_kernel() {}
+
+int launch_floor(int device, int reps, double* us) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e) return (int)e;
+    cudaStream_t st;
+    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking))) return (int)e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int i = 0; i < 16; ++i) empty_kernel<<<1, 32, 0, st>>>();
+    cudaEventRecord(a, st);
+    for (int i = 0; i < reps; ++i) empty_kernel<<<1, 32, 0, st>>>();
+    cudaEventRecord(b, st);
+    e = cudaEventSynchronize(b);
+    float ms = 0;
+    if (!e) e = cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    if (e) return (int)e;
+    *us = 1e3 * ms / reps;
+    return 0;
 }
 
 int fp64_probe(int device, double* tflops) {

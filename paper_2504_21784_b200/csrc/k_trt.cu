@@ -173,20 +173,23 @@ __device__ __forceinline__ void emission_sum_warp(double T, int G, const double*
 }
 
 // per node (one warp): solve cv_dt (T - Tk) + E(T) = sphi by a bracketed Newton
-// iteration from the current iterate T; writes the new T and per-block partial sums of
-// (dT^2, T^2) for the convergence test (summed in a fixed order afterwards).  One warp
+// iteration from the current iterate T; writes the new T, replaces the previous energy
+// density E^l by this sweep's phi, and writes per-block partial sums of (dT^2, dE^2) for
+// the outer stopping test ||u^{l+1} - u^l||_2 < eps ||u^1 - u^0||_2, u = [T, E]
+// (eq:relative_tol), summed in a fixed order afterwards.  One warp
 // per node: nodes converge after different numbers of steps, and a thread per node
 // made every warp wait for its slowest node.
 #ifndef SWEEP_TRT_MINB
 #define SWEEP_TRT_MINB 3  // 72 registers, 3 blocks of 256 per SM, grid 3 x 148: C5 TRT 23.9 -> 23.4 ms
 #endif
 __global__ void __launch_bounds__(256, SWEEP_TRT_MINB) trt_update_kernel(const double* __restrict__ Tk, double* __restrict__ T,
-                                                         const double* __restrict__ sphi, const double* __restrict__ sigma,
+                                                         const double* __restrict__ sphi, const double* __restrict__ phi,
+                                                         double* __restrict__ E, const double* __restrict__ sigma,
                                                          const double* __restrict__ nu, int G, int n, size_t nodes,
                                                          double cv_dt, double* __restrict__ partial, int* err) {
     __shared__ double red[2][8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double dsq = 0.0, tsq = 0.0;
+    double dsq = 0.0, esq = 0.0;
     const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
     for (size_t v = (size_t)blockIdx.x * (blockDim.x >> 5) + wib; v < nodes; v += warps) {
         const double* sg = sigma + (v / n) * G;
@@ -244,12 +247,15 @@ __global__ void __launch_bounds__(256, SWEEP_TRT_MINB) trt_update_kernel(const d
             if (!ok || !(t > 0.0) || !(t < 1e300)) atomicOr(err, 16);
             T[v] = t;
             dsq = fma(t - told, t - told, dsq);
-            tsq = fma(t, t, tsq);
+            // E = phi (c = 1): the energy-density half of u = [T, E] (eq:relative_tol)
+            const double en = phi[v], de = en - E[v];
+            E[v] = en;
+            esq = fma(de, de, esq);
         }
     }
     if (lane == 0) {
         red[0][wib] = dsq;
-        red[1][wib] = tsq;
+        red[1][wib] = esq;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -279,21 +285,44 @@ __global__ void trt_norm_kernel(const double* __restrict__ partial, int nblocks,
 #ifndef SWEEP_TRT_BPS
 #define SWEEP_TRT_BPS 3
 #endif
-int trt_blocks() { return 148 * SWEEP_TRT_BPS; }
+int trt_blocks(int n_sm) { return (n_sm > 0 ? n_sm : 1) * SWEEP_TRT_BPS; }
 
 int launch_trt_emission(const double* T, const double* sigma, const double* Iprev, const double* nu, int G, int n,
-                        size_t nodes, double inv_dt, double* q, void* stream) {
+                        size_t nodes, double inv_dt, double* q, int n_sm, void* stream) {
 #ifndef SWEEP_EMIS_BPS
 #define SWEEP_EMIS_BPS 4  // all blocks resident (a grid-stride kernel: 8 x 148 left a partial second wave; -0.5 ms)
 #endif
-    trt_emission_kernel<<<148 * SWEEP_EMIS_BPS, 256, 0, (cudaStream_t)stream>>>(T, sigma, Iprev, nu, G, n, nodes, inv_dt, q);
+    trt_emission_kernel<<<(n_sm > 0 ? n_sm : 1) * SWEEP_EMIS_BPS, 256, 0, (cudaStream_t)stream>>>(T, sigma, Iprev, nu, G, n, nodes, inv_dt, q);
     return (int)cudaGetLastError();
 }
 
-int launch_trt_update(const double* Tk, double* T, const double* sphi, const double* sigma, const double* nu, int G,
-                      int n, size_t nodes, double cv_dt, double* partial, double* norms, int* err, void* stream) {
-    const int nb = trt_blocks();
-    trt_update_kernel<<<nb, 256, 0, (cudaStream_t)stream>>>(Tk, T, sphi, sigma, nu, G, n, nodes, cv_dt, partial, err);
+// E^0 = sum_g I^k_g at every node (the energy density of the isotropic previous
+// intensity: c = 1, sum_d w_d = 1), the E half of the initial guess u^0 = [T^k, E^k];
+// one thread per node, groups summed in index order
+__global__ void trt_e0_kernel(const double* __restrict__ Iprev, int G, size_t nodes, double* __restrict__ E) {
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += (size_t)gridDim.x * blockDim.x) {
+        const double* I = Iprev + v * (size_t)G;
+        double e = 0.0;
+        for (int g = 0; g < G; ++g) e += I[g];
+        E[v] = e;
+    }
+}
+
+int launch_trt_e0(const double* Iprev, int G, size_t nodes, double* E, int n_sm, void* stream) {
+    const int block = 256;
+    size_t want = (nodes + block - 1) / block;
+    const size_t cap = (size_t)n_sm * 8;
+    const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+    trt_e0_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(Iprev, G, nodes, E);
+    return (int)cudaGetLastError();
+}
+
+int launch_trt_update(const double* Tk, double* T, const double* sphi, const double* phi, double* E,
+                      const double* sigma, const double* nu, int G, int n, size_t nodes, double cv_dt, double* partial,
+                      double* norms, int* err, int n_sm, void* stream) {
+    const int nb = trt_blocks(n_sm);
+    trt_update_kernel<<<nb, 256, 0, (cudaStream_t)stream>>>(Tk, T, sphi, phi, E, sigma, nu, G, n, nodes, cv_dt, partial,
+                                                            err);
     trt_norm_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(partial, nb, norms);
     return (int)cudaGetLastError();
 }

@@ -36,6 +36,12 @@
 
 #include "sweep_internal.h"
 
+// ablation switches give wrong results by design (timing experiments only)
+#if (defined(SWEEP_ABL_NOPHASEC) || defined(SWEEP_ABL_NOWAIT) || defined(SWEEP_ABL_NOYTR) || \
+     defined(SWEEP_ABL_NORED)) && !defined(SWEEP_EXPERIMENTS)
+#error "SWEEP_ABL_* switches are for experiment builds only (scripts/build_variants.py)"
+#endif
+
 namespace sweepk {
 
 static __constant__ ModalConsts cM;  // per translation unit
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
     constexpr int T = rows_per_strip(P, K);
     constexpr int C = cols_per_chunk(P, K, OPT);
     constexpr int CT = C * T;
-    constexpr int NFIELD = 14;  // 6 moments + (beta, J+) x 4 faces
+    constexpr int NFIELD = 16;  // 6 moments + (beta, J+) x 4 faces + untraced P_xx, P_yy weights
 
     const int NL = blockDim.x;
     const int tid = threadIdx.x;
@@ -633,6 +639,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         double* coefS = S + (size_t)CT * SEL;
         double* ypre = coefS + dset * NFIELD;  // [K*NT][NL] next-column trace prefetch
         constexpr int NFO = SIG ? 9 : 6;       // node fields: 6 moments (+ sigma phi, sigma Jx, sigma Jy)
+        // SWEEP_HALF_RANGE: + the untraced P_xx, P_yy = sum w Omega_x^2 psi, sum w Omega_y^2 psi of
+        // this stream (quadrant), into the stream slab's half-range rows (read by halfrange_kernel;
+        // forming them as T + phi/3 there cancels when Omega^2 << 1/3)
+        const int nfo = NFO + (prm.half ? 2 : 0);
         double* bckS = ypre + K * NT * NL;     // [9][9] modal -> nodal (p = 2, boundary closures)
         double* S2 = bckS + 81;                // SIG: [CT][SEL] sigma-weighted group sums
 #ifndef SWEEP_DEFER_C
@@ -658,7 +668,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             double v = 0.0;
             if (dd < sd.nd) {
                 const DirConst* D = prm.dirs + sd.d0 + dd;
-                v = (f < 6) ? D->mom[f] : (((f - 6) & 1) ? D->jw[(f - 6) >> 1] : D->bw[(f - 6) >> 1]);
+                v = (f < 6) ? D->mom[f] : (f >= 14) ? D->pw[f - 14] : (((f - 6) & 1) ? D->jw[(f - 6) >> 1] : D->bw[(f - 6) >> 1]);
             }
             coefS[it] = v;
         }
@@ -711,7 +721,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                 // field f < 6: the moments from S; SIG f = 6, 7, 8: sigma phi, sigma Jx,
                 // sigma Jy from S2 with the weights of phi, Jx, Jy
                 auto field_dst = [&](int f) -> double* {
-                    return slab + ((f < 6) ? (size_t)f * nodes : sig_off + (size_t)(f - 6) * nodes);
+                    return slab + ((f < 6)     ? (size_t)f * nodes
+                                   : (f < NFO) ? sig_off + (size_t)(f - 6) * nodes
+                                               : prm.hr_off + (size_t)(f - NFO) * nodes);
                 };
                 // PC outputs per thread per pass: independent accumulation chains, and all
                 // their S loads ahead of the stores (Mbuf and S share the smem window)
@@ -719,17 +731,17 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #define SWEEP_PC 1  // 4 (0.3 % faster at C5) hits an illegal-instruction fault in the p = 2, 2-lane layout with modal slabs
 #endif
                 constexpr int PC = SWEEP_PC;
-                for (int o0 = tid; o0 < CT * NFO * NQ; o0 += PC * NL) {
+                for (int o0 = tid; o0 < CT * nfo * NQ; o0 += PC * NL) {
                     const double* Sp[PC];
                     const double* cf[PC];
                     double acc[PC];
 #pragma unroll
                     for (int u = 0; u < PC; ++u) {
-                        const int o = min(o0 + u * NL, CT * NFO * NQ - 1);
+                        const int o = min(o0 + u * NL, CT * nfo * NQ - 1);
                         const int m = o % NQ, rest = o / NQ;
-                        const int f = rest % NFO, el = rest / NFO;
-                        Sp[u] = ((f < 6) ? S : S2) + (size_t)el * SEL + m;
-                        cf[u] = coefS + ((f < 6) ? f : f - 6);
+                        const int f = rest % nfo, el = rest / nfo;
+                        Sp[u] = ((f < 6 || f >= NFO) ? S : S2) + (size_t)el * SEL + m;
+                        cf[u] = coefS + ((f < 6) ? f : (f < NFO) ? f - 6 : 14 + (f - NFO));
                         acc[u] = 0.0;
                     }
                     for (int dd = 0; dd < sd.nd; ++dd) {
@@ -739,9 +751,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                     for (int u = 0; u < PC; ++u) {
                         const int o = o0 + u * NL;
-                        if (o >= CT * NFO * NQ) continue;
+                        if (o >= CT * nfo * NQ) continue;
                         const int m = o % NQ, rest = o / NQ;
-                        const int f = rest % NFO, el = rest / NFO;
+                        const int f = rest % nfo, el = rest / nfo;
                         const int col = el / T, r = el - col * T;
                         if (col < cols && r < rows) {
                             const int ip = i0 + col, jp = j0 + r;
@@ -1265,6 +1277,7 @@ template <int P, int LOG2GB, int OPT>
 __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) {
     constexpr bool SIG = (OPT & OPT_SIGMA) != 0;  // + sigma phi, sigma J (NEXT-1)
     constexpr bool FIX = (OPT & OPT_FIXUP) != 0;  // zero-and-scale fixup (NEXT-2); host runs one segment
+    constexpr bool HALF = (OPT & OPT_HALF) != 0;  // + untraced P_xx = sum w mu^2 psi of this half-range (NEXT-3)
     constexpr int NP1 = P + 1;
     constexpr int GB = 1 << LOG2GB;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -1277,13 +1290,14 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
     extern __shared__ __align__(16) double sm1[];
     double* TS = sm1;                       // [nseg][32][2]
     double* IN = TS + prm.nseg * 64;        // [nseg][32]
-    double c = 0.0, cm0 = 0.0, cm1 = 0.0, cm2 = 0.0, bw0 = 0.0, bw1 = 0.0, jw0 = 0.0, jw1 = 0.0;
+    double c = 0.0, cm0 = 0.0, cm1 = 0.0, cm2 = 0.0, cp = 0.0, bw0 = 0.0, bw1 = 0.0, jw0 = 0.0, jw1 = 0.0;
     if (d_on && g_on) {
         const DirConst& D = prm.dirs[sd.d0 + dl];
         c = D.cx;
         cm0 = D.mom[0];
         cm1 = D.mom[1];
         cm2 = D.mom[2];
+        cp = D.pw[0];
         bw0 = D.bw[0];
         bw1 = D.bw[1];
         jw0 = D.jw[0];
@@ -1354,7 +1368,8 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
         }
         up = psi[P];
         const int i = fx ? nx - 1 - ip : ip;
-        constexpr int NV = (SIG ? 5 : 3) * NP1;  // phi, J, Txx (+ sigma phi, sigma J)
+        constexpr int NM = SIG ? 5 : 3;                  // phi, J, Txx (+ sigma phi, sigma J)
+        constexpr int NV = (NM + (HALF ? 1 : 0)) * NP1;  // (+ P_xx)
         double v[NV];
 #pragma unroll
         for (int aq = 0; aq < NP1; ++aq) {
@@ -1365,13 +1380,16 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
                 v[3 * NP1 + aq] = sg * v[0 * NP1 + aq];
                 v[4 * NP1 + aq] = sg * v[1 * NP1 + aq];
             }
+            if constexpr (HALF) v[NM * NP1 + aq] = cp * psi[aq];
         }
         const size_t sig_off = 3 * nodes + 4;  // after phi, J, Txx, beta[2], J+[2]
         auto sink = [&](int idx, double val) {
             if (idx < NV) {
                 const int m = idx / NP1, aq = idx - m * NP1;
                 const int a = fx ? P - aq : aq;
-                const size_t base = (m < 3) ? (size_t)m * nodes : sig_off + (size_t)(m - 3) * nodes;
+                const size_t base = (m < 3)    ? (size_t)m * nodes
+                                    : (m < NM) ? sig_off + (size_t)(m - 3) * nodes
+                                               : prm.hr_off;
                 slab[base + (size_t)i * NP1 + a] = val;
             }
         };

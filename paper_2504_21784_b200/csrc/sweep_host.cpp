@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +18,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (ranges are no-ops without a profiler attached)
 
 #include "../../include/sweep.h"
 #include "sweep_internal.h"
@@ -73,6 +76,12 @@ NcclApi g_nccl;
 thread_local std::string g_setup_error;
 constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
+// NVTX range for the lifetime of a scope (setup, run, all-reduce, closures, TRT iterations)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct DeviceGuard {
     int prev = -1;
     bool ok = false;
@@ -97,6 +106,8 @@ struct sweep_handle {
     // schedule
     int log2gb, gb, kpl, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
     size_t smem;
+    int n_sm = 0;                 // SMs of the handle's device (queried at setup)
+    sweepk::ReduceCaps caps{};    // grid caps of the reduction kernels
     // device workspace
     DirConst* d_dirs = nullptr;
     StreamDesc* d_streams = nullptr;
@@ -111,6 +122,7 @@ struct sweep_handle {
     double *d_in_sigma = nullptr, *d_in_q = nullptr, *d_in_inflow = nullptr;
     // unaccelerated TRT iteration workspace (trt_step)
     double *d_trt_q = nullptr, *d_trt_nu = nullptr, *d_trt_part = nullptr, *d_trt_norm = nullptr;
+    double* d_trt_E = nullptr;  // E^l of the outer iteration (eq:relative_tol, u = [T, E])
     int trt_nu_len = 0;
     ncclComm_t comm = nullptr;
     long long launches = 0;
@@ -298,6 +310,7 @@ extern "C" int sweep_nccl_unique_id(void* out128) {
 }
 
 extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
+    NvtxRange nv("sweep_setup");
     if (out) *out = nullptr;
     if (!desc || !out || !desc->omega || !desc->w) return fail(nullptr, SWEEP_E_ARG, "null pointer");
     const sweep_desc& D = *desc;
@@ -424,6 +437,8 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             c.bw[f] = d.w * (std::fabs(on[f]) - alpha[f]);
             c.jw[f] = d.w * std::max(on[f], 0.0);
         }
+        c.pw[0] = d.w * (d.ox * d.ox);
+        c.pw[1] = d.w * (d.oy * d.oy);
         byq[q].push_back(c);
     }
     std::vector<DirConst> table;
@@ -456,7 +471,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->gb = gbw;
         h->log2gb = ilog2_ceil(gbw);
     }
-    // experiment override (2-D only): SWEEP_CFG="K,LG" with K in {1,2,4}, LG a power of two <= 32
+#ifdef SWEEP_EXPERIMENTS
+    // experiment builds only (scripts/build_variants.py): SWEEP_CFG="K,LG" with K in {1,2,4},
+    // LG a power of two <= 32 overrides the 2-D lane layout
     if (D.dim == 2) {
         if (const char* ev = getenv("SWEEP_CFG")) {
             int k = 0, lg = 0;
@@ -468,6 +485,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             }
         }
     }
+#endif
     const int gbk = h->gb * h->kpl;
     const int n_gblocks = (h->G + gbk - 1) / gbk;
     const int dirs_per_warp = 32 / h->gb;
@@ -476,7 +494,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     std::vector<StreamDesc> streams;
     if (D.dim == 2) {
         int max_warps = 8;
-        if (const char* ev = getenv("SWEEP_MAXWARPS")) max_warps = std::max(1, std::min(8, atoi(ev)));  // experiment override
+#ifdef SWEEP_EXPERIMENTS
+        if (const char* ev = getenv("SWEEP_MAXWARPS")) max_warps = std::max(1, std::min(8, atoi(ev)));
+#endif
         const int nw = std::min(max_warps, std::max(1, (maxq + dirs_per_warp - 1) / dirs_per_warp));
         h->block = 32 * nw;
         h->dset = nw * dirs_per_warp;
@@ -528,6 +548,15 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
 
     // schedule + workspace
     cudaError_t ce;
+    if ((ce = cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device)) || h->n_sm < 1) {
+        if (!ce) ce = cudaErrorInvalidDevice;
+        cuda_fail(h, ce, "SM count");
+        return bail(SWEEP_E_CUDA);
+    }
+    if (int re = sweepk::reduce_caps(h->n_sm, &h->caps)) {
+        cuda_fail(h, (cudaError_t)re, "occupancy of the reduction kernels");
+        return bail(SWEEP_E_CUDA);
+    }
     if (D.dim == 2) {
         const int T = sweepk::sweep2d_rows_per_strip(h->p, h->kpl), C = sweepk::sweep2d_cols_per_chunk(h->p, h->kpl, h->opt);
         h->n_strips = (h->ny + T - 1) / T;
@@ -541,9 +570,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             else h->err = "sweep2d kernel cannot be resident (registers/shared memory)";
             return bail(SWEEP_E_CUDA);
         }
-        int nsm = 0;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-        h->grid = std::min(h->n_tasks, bps * std::max(nsm, 1));
+        h->grid = std::min(h->n_tasks, bps * h->n_sm);
         const int NT = h->np1;
         h->progress_ints = (size_t)h->n_streams * h->n_strips;
         if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * (size_t)h->n_streams * 2 * (h->n_chunks * C) * h->kpl * NT * h->block)))
@@ -578,10 +605,9 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     if ((ce = cudaMalloc(&h->d_out, sizeof(double) * h->out_size)))
         return cuda_fail(h, ce, "cudaMalloc out"), bail(SWEEP_E_CUDA);
 
-    // NCCL for nranks > 1; SWEEP_FORCE_NCCL=1 (tests) also builds a 1-rank communicator
-    // when an id is given, so the NCCL plumbing runs on a single-GPU box
-    const char* force = getenv("SWEEP_FORCE_NCCL");
-    if (h->nranks > 1 || (force && force[0] == '1' && D.nccl_id)) {
+    // NCCL for nranks > 1; SWEEP_FORCE_COMM also builds a 1-rank communicator when an id is
+    // given, so the NCCL plumbing can run on a single-GPU box
+    if (h->nranks > 1 || ((D.flags & SWEEP_FORCE_COMM) && D.nccl_id)) {
         std::string e;
         if (!g_nccl.load(e)) {
             h->err = e;
@@ -609,6 +635,7 @@ extern "C" int sweep_layout(const sweep_handle* h, size_t off[8], size_t* total)
 
 extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt, const double* d_q,
                          const double* d_inflow, void* stream) {
+    NvtxRange nv("sweep_run");
     if (!h) return SWEEP_E_ARG;
     if (!d_sigma || !d_q || !d_inflow) return fail(h, SWEEP_E_ARG, "null input pointer");
     if (!std::isfinite(inv_c_dt) || !(inv_c_dt > 0)) return fail(h, SWEEP_E_ARG, "inv_c_dt must be finite and > 0");
@@ -632,7 +659,12 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.ny = h->ny;
         prm.G = h->G;
         prm.nx_pad = h->n_chunks * sweepk::sweep2d_cols_per_chunk(h->p, h->kpl, h->opt);
-        prm.bulk_ok = (h->G % 2 == 0) ? 1 : 0;
+        // 1-D bulk copies (cp.async.bulk) of the q / sigma group rows need 16-byte aligned
+        // rows: G even (the group offsets of the streams are even then) and aligned bases
+        prm.bulk_ok = (h->G % 2 == 0 && (reinterpret_cast<uintptr_t>(d_q) & 15u) == 0 &&
+                       (reinterpret_cast<uintptr_t>(d_sigma) & 15u) == 0)
+                          ? 1
+                          : 0;
         prm.n_streams = h->n_streams;
         prm.n_strips = h->n_strips;
         prm.n_chunks = h->n_chunks;
@@ -641,6 +673,8 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.kpl = h->kpl;
         prm.dset = h->dset;
         prm.nbnode = h->nbnode;
+        prm.half = (h->flags & SWEEP_HALF_RANGE) ? 1 : 0;
+        prm.hr_off = h->off[7];
         prm.inv_c_dt = inv_c_dt;
         prm.sigma = d_sigma;
         prm.q = d_q;
@@ -663,6 +697,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.gb = h->gb;
         prm.nseg = h->nseg;
         prm.seglen = h->seglen;
+        prm.hr_off = h->off[7];
         prm.inv_c_dt = inv_c_dt;
         prm.sigma = d_sigma;
         prm.q = d_q;
@@ -673,38 +708,41 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.out_size = h->out_size;
         prm.nodes = h->nodes;
         prm.err = h->d_err;
-        e = sweepk::launch_sweep1d(h->p, h->log2gb, h->opt, prm, h->grid, h->block, h->smem, stream);
+        const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
+        e = sweepk::launch_sweep1d(h->p, h->log2gb, opt1, prm, h->grid, h->block, h->smem, stream);
     }
     if (e) return cuda_fail(h, (cudaError_t)e, "launch sweep");
     ++h->launches;
     if (evs) cudaEventRecord(evs[1], st);
     const bool modal = (h->dim == 2 && h->p == 2);  // the p = 2 sweep leaves modal node fields in the slabs
     if (!modal) {
-        e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->sum_size, h->d_out, h->d_err, stream);
+        e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->sum_size, h->d_out, h->d_err,
+                                    h->caps.finalize, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");
         ++h->launches;
     } else {
         const size_t nel = h->nodes / 9;
         // phi, J, T rows | beta, J+ (plain sum) | sigma phi, sigma J rows (SWEEP_SIGMA_MOMENTS)
         e = sweepk::launch_finalize_modal(h->d_slabs, h->n_streams, h->out_size, h->d_streams, 0, 6, nel, h->d_out,
-                                          h->d_err, stream);
+                                          h->d_err, h->caps.finalize_modal, stream);
         if (!e)
             e = sweepk::launch_finalize(h->d_slabs + h->off[3], h->n_streams, h->out_size, 2 * (size_t)h->nbnode,
-                                        h->d_out + h->off[3], h->d_err, stream);
+                                        h->d_out + h->off[3], h->d_err, h->caps.finalize, stream);
         if (!e && h->off[7] > h->off[5])
             e = sweepk::launch_finalize_modal(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->off[5], 3, nel,
-                                              h->d_out, h->d_err, stream);
+                                              h->d_out, h->d_err, h->caps.finalize_modal, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");
         h->launches += (h->off[7] > h->off[5]) ? 3 : 2;
     }
     if (h->out_size > h->sum_size) {
-        e = sweepk::launch_halfrange(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->nodes, h->dim, modal ? 1 : 0,
-                                     h->d_out + h->sum_size, stream);
+        e = sweepk::launch_halfrange(h->d_slabs, h->n_streams, h->out_size, h->d_streams, h->nodes, h->off[7], h->dim,
+                                     modal ? 1 : 0, h->d_out + h->sum_size, h->caps.halfrange, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch halfrange");
         ++h->launches;
     }
     if (evs) cudaEventRecord(evs[2], st);
     if (h->comm) {
+        NvtxRange nva("sweep_allreduce");
         int r = g_nccl.allReduce(h->d_out, h->d_out, h->out_size, kNcclFloat64, kNcclSum, h->comm, st);
         if (r != 0)
             return fail(h, SWEEP_E_NCCL, std::string("ncclAllReduce: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
@@ -763,6 +801,7 @@ extern "C" int sweep_fp64_probe(int device, double* tflops) {
 }
 
 extern "C" int closures_get(sweep_handle* h, double* out, size_t n, void* stream) {
+    NvtxRange nv("closures_get");
     if (!h || !out) return SWEEP_E_ARG;
     if (n != h->out_size) return fail(h, SWEEP_E_ARG, "n_doubles must equal the layout total");
     DeviceGuard guard(h->device);
@@ -820,30 +859,43 @@ extern "C" int trt_step(sweep_handle* h, const double* d_sigma, const double* d_
     if (!h->d_trt_q) {
         if ((ce = cudaMalloc(&h->d_trt_q, sizeof(double) * nq))) return cuda_fail(h, ce, "cudaMalloc trt q");
         if ((ce = cudaMalloc(&h->d_trt_nu, sizeof(double) * (h->G + 1)))) return cuda_fail(h, ce, "cudaMalloc trt nu");
-        if ((ce = cudaMalloc(&h->d_trt_part, sizeof(double) * 2 * sweepk::trt_blocks())))
+        if ((ce = cudaMalloc(&h->d_trt_part, sizeof(double) * 2 * sweepk::trt_blocks(h->n_sm))))
             return cuda_fail(h, ce, "cudaMalloc trt partials");
         if ((ce = cudaMalloc(&h->d_trt_norm, sizeof(double) * 2))) return cuda_fail(h, ce, "cudaMalloc trt norms");
+        if ((ce = cudaMalloc(&h->d_trt_E, sizeof(double) * h->nodes))) return cuda_fail(h, ce, "cudaMalloc trt E");
     }
     if ((ce = cudaMemcpyAsync(h->d_trt_nu, prm->nu, sizeof(double) * (h->G + 1), cudaMemcpyHostToDevice, st)))
         return cuda_fail(h, ce, "copy nu");
     if ((ce = cudaMemcpyAsync(d_T, d_Tk, sizeof(double) * h->nodes, cudaMemcpyDeviceToDevice, st)))
         return cuda_fail(h, ce, "copy Tk");
+    // u^0 = [T^k, E^k], E^k = sum_g I^k_g
+    if (int e0 = sweepk::launch_trt_e0(d_Iprev, h->G, h->nodes, h->d_trt_E, h->n_sm, stream))
+        return cuda_fail(h, (cudaError_t)e0, "launch trt E0");
     const double inv_dt = 1.0 / prm->dt, cv_dt = prm->cv / prm->dt;
+    // outer stopping rule (eq:relative_tol): stop after the first
+    // iteration l >= 2 with ||u^l - u^{l-1}||_2 < eps ||u^1 - u^0||_2, u = [T, E = phi];
+    // after iteration 1 if u^1 = u^0 exactly
+    double first = 0.0;
     int it = 0;
     for (it = 1; it <= prm->max_iter; ++it) {
+        NvtxRange nvi("trt_outer_iteration");
         int e = sweepk::launch_trt_emission(d_T, d_sigma, d_Iprev, h->d_trt_nu, h->G, h->n, h->nodes, inv_dt, h->d_trt_q,
-                                            stream);
+                                            h->n_sm, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch trt emission");
         int rc = sweep_run(h, d_sigma, inv_dt, h->d_trt_q, d_inflow, stream);
         if (rc) return rc;
-        e = sweepk::launch_trt_update(d_Tk, d_T, h->d_out + h->off[5], d_sigma, h->d_trt_nu, h->G, h->n, h->nodes, cv_dt,
-                                      h->d_trt_part, h->d_trt_norm, h->d_err, stream);
+        e = sweepk::launch_trt_update(d_Tk, d_T, h->d_out + h->off[5], h->d_out + h->off[0], h->d_trt_E, d_sigma,
+                                      h->d_trt_nu, h->G, h->n, h->nodes, cv_dt, h->d_trt_part, h->d_trt_norm, h->d_err,
+                                      h->n_sm, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch trt update");
         double norms[2] = {0.0, 0.0};
         if ((ce = cudaMemcpyAsync(norms, h->d_trt_norm, sizeof norms, cudaMemcpyDeviceToHost, st)))
             return cuda_fail(h, ce, "copy norms");
         if ((ce = cudaStreamSynchronize(st))) return cuda_fail(h, ce, "sync");
-        if (prm->eps > 0 && std::sqrt(norms[0]) <= prm->eps * std::sqrt(norms[1])) break;
+        const double dn = std::sqrt(norms[0] + norms[1]);
+        if (it == 1) first = dn;
+        if (prm->ratios) prm->ratios[it - 1] = (first > 0.0) ? dn / first : 0.0;
+        if (prm->eps > 0 && (first == 0.0 || (it >= 2 && dn < prm->eps * first))) break;
     }
     *iterations = std::min(it, prm->max_iter);
     int flag = 0;
@@ -856,12 +908,26 @@ extern "C" int trt_step(sweep_handle* h, const double* d_sigma, const double* d_
     return SWEEP_OK;
 }
 
-extern "C" int sweep_stats(const sweep_handle* h, long long out[4]) {
+extern "C" int sweep_stats(const sweep_handle* h, long long out[8]) {
     if (!h || !out) return SWEEP_E_ARG;
     out[0] = h->launches;
     out[1] = h->n_dir_eff;
     out[2] = h->n_streams;
     out[3] = h->grid;
+    out[4] = h->block;
+    out[5] = (h->dim == 2) ? h->kpl : 1;
+    out[6] = h->gb;
+    out[7] = h->n_sm;
+    return SWEEP_OK;
+}
+
+extern "C" int sweep_launch_floor(int device, int reps, double* us_per_launch) {
+    if (!us_per_launch || reps < 1) return SWEEP_E_ARG;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    int e = sweepk::launch_floor(device, reps, us_per_launch);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (e) return fail(nullptr, SWEEP_E_CUDA, std::string("launch floor: ") + sweepk::cuda_err_string(e));
     return SWEEP_OK;
 }
 
@@ -876,6 +942,7 @@ extern "C" void sweep_destroy(sweep_handle* h) {
     cudaFree(h->d_trt_nu);
     cudaFree(h->d_trt_part);
     cudaFree(h->d_trt_norm);
+    cudaFree(h->d_trt_E);
     cudaFree(h->d_progress);
     cudaFree(h->d_ytr);
     cudaFree(h->d_slabs);

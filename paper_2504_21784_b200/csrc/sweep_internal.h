@@ -9,6 +9,8 @@ namespace sweepk {
 // compile-time kernel options (template parameter OPT)
 constexpr int OPT_SIGMA = 1;   // append sum_g sigma_g phi_g, sum_g sigma_g J_g
 constexpr int OPT_FIXUP = 2;   // zero-and-scale negative flux fixup inside the sweep (NEXT-2)
+constexpr int OPT_HALF = 4;    // 1-D: also the untraced P_xx row of each half-range stream (NEXT-3);
+                               // 2-D takes this at run time (Sweep2DParams::half)
 
 // Per (folded) direction, in sweep coordinates (every direction is mapped to
 // the (+,+) quadrant by mirroring the element order and the nodes).
@@ -19,6 +21,7 @@ struct DirConst {
                        //  1-D: w, w mu, w(mu^2-1/3), 0, 0, 0
     double bw[4];      // beta weights per physical face x-,x+,y-,y+: w(|Omega.n| - alpha_n)
     double jw[4];      // J+ weights per physical face: w max(Omega.n, 0)
+    double pw[2];      // untraced second-moment weights w Omega_x^2, w Omega_y^2 (half-range P+, NEXT-3)
 };
 
 // One work stream = (quadrant, group block, direction set): the lanes of one CTA.
@@ -53,6 +56,8 @@ struct Sweep2DParams {
     int dset;                      // directions per CTA
     int nbnode;
     int bulk_ok;                   // q / sigma rows are 16-byte aligned (G even): 1-D bulk copies
+    int half;                      // SWEEP_HALF_RANGE: write the P_xx, P_yy rows at hr_off of the slab
+    size_t hr_off;
     double inv_c_dt;
     const double* sigma;           // [N_el][G]
     const double* q;               // [N_el][n][G]
@@ -70,6 +75,7 @@ struct Sweep2DParams {
 
 struct Sweep1DParams {
     int nx, G, n_streams, gb, nseg, seglen;
+    size_t hr_off;                 // OPT_HALF: slab offset of the P_xx row
     double inv_c_dt;
     const double* sigma;
     const double* q;
@@ -87,25 +93,34 @@ int upload_modal(const ModalConsts& mc);
 int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, int grid, int block, size_t smem,
                    void* stream);
 int launch_sweep1d(int p, int log2gb, int opt, const Sweep1DParams& prm, int grid, int block, size_t smem, void* stream);
-int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, void* stream);
-int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes, int dim,
-                     int modal, double* out, void* stream);
+// grid caps (SMs x resident blocks per SM) of the grid-stride reduction kernels, per handle
+struct ReduceCaps {
+    int finalize, finalize_modal, halfrange;
+};
+int reduce_caps(int n_sm, ReduceCaps* caps);
+int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, int cap,
+                    void* stream);
+int launch_halfrange(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t nodes,
+                     size_t hr_off, int dim, int modal, double* out, int cap, void* stream);
 // 2-D p = 2: back transform + fixed-order sum of the modal node-field rows [row0, row0 + nrows*nel*9)
 int launch_finalize_modal(const double* slabs, int n_slabs, size_t stride, const StreamDesc* streams, size_t row0,
-                          int nrows, size_t nel, double* out, int* err, void* stream);
+                          int nrows, size_t nel, double* out, int* err, int cap, void* stream);
 int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt);
 int sweep2d_occupancy(int p, int log2lg, int k, int opt, int block, size_t smem, int* blocks_per_sm);
 int sweep2d_rows_per_strip(int p, int k);
 int sweep2d_cols_per_chunk(int p, int k, int opt);
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
+int launch_floor(int device, int reps, double* us);
 
 // unaccelerated TRT iteration (k_trt.cu)
-int trt_blocks();
+int trt_blocks(int n_sm);
 int launch_trt_emission(const double* T, const double* sigma, const double* Iprev, const double* nu, int G, int n,
-                        size_t nodes, double inv_dt, double* q, void* stream);
-int launch_trt_update(const double* Tk, double* T, const double* sphi, const double* sigma, const double* nu, int G,
-                      int n, size_t nodes, double cv_dt, double* partial, double* norms, int* err, void* stream);
+                        size_t nodes, double inv_dt, double* q, int n_sm, void* stream);
+int launch_trt_e0(const double* Iprev, int G, size_t nodes, double* E, int n_sm, void* stream);
+int launch_trt_update(const double* Tk, double* T, const double* sphi, const double* phi, double* E,
+                      const double* sigma, const double* nu, int G, int n, size_t nodes, double cv_dt, double* partial,
+                      double* norms, int* err, int n_sm, void* stream);
 
 // per translation unit (k2d_*.cu): kernel pointer for (log2lg, k, opt), or nullptr;
 // and the upload of that unit's copy of the modal constants

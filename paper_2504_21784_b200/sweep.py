@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SWEEP_LIB") or os.path.join(_HERE, "libsweep.so")  # SWEEP_LIB: experiment builds only
+LIB_PATH = os.path.join(_HERE, "libsweep.so")
 
 SWEEP_OK, E_ARG, E_QUAD, E_SIGMA, E_CUDA, E_NCCL, E_INTERNAL = range(7)
 FOLD_Z = 1
@@ -20,12 +20,13 @@ DETERMINISTIC = 2
 SIGMA_MOMENTS = 4   # also return sum_g sigma_g phi_g, sum_g sigma_g J_g (NEXT-1)
 FIXUP = 8           # zero-and-scale negative flux fixup inside the sweep (NEXT-2)
 HALF_RANGE = 16     # also return the half-range moments F+, P+ of the consistent method (NEXT-3)
+FORCE_COMM = 32     # nranks = 1 with a nccl_id: still run the (1-rank) NCCL all-reduce (plumbing tests)
 _NAMES = {1: "E_ARG", 2: "E_QUAD", 3: "E_SIGMA", 4: "E_CUDA", 5: "E_NCCL", 6: "E_INTERNAL"}
 
 # every symbol include/sweep.h declares
 EXPORTS = ("sweep_setup", "sweep_layout", "sweep_run", "closures_get", "sweep_run_host", "trt_step",
            "sweep_stats", "sweep_timing", "sweep_kernel_times", "sweep_fp64_probe",
-           "sweep_nccl_unique_id", "sweep_destroy", "sweep_last_error")
+           "sweep_nccl_unique_id", "sweep_destroy", "sweep_last_error", "sweep_launch_floor")
 
 
 class SweepError(RuntimeError):
@@ -46,15 +47,20 @@ class sweep_desc(ctypes.Structure):
 
 class trt_params(ctypes.Structure):
     _fields_ = [("nu", ctypes.POINTER(ctypes.c_double)), ("cv", ctypes.c_double), ("dt", ctypes.c_double),
-                ("eps", ctypes.c_double), ("max_iter", ctypes.c_int)]
+                ("eps", ctypes.c_double), ("max_iter", ctypes.c_int), ("ratios", ctypes.POINTER(ctypes.c_double))]
 
 
 _lib = None
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libsweep.so (fails loudly if it has not been built)."""
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Load libsweep.so (fails loudly if it has not been built).  `path` selects another
+    build of the same library (experiment builds, scripts/build_variants.py); it must be
+    given before the first load."""
     global _lib
+    if _lib is not None and path is not None and os.path.abspath(path) != _lib._name_abs:
+        raise RuntimeError(f"libsweep already loaded from {_lib._name_abs}")
+    path = path or LIB_PATH
     if _lib is None:
         if not os.path.exists(path):
             raise RuntimeError(f"{path} not built: run `python -m paper_2504_21784_b200.build` "
@@ -81,12 +87,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.sweep_kernel_times.restype = i
         lib.sweep_fp64_probe.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
         lib.sweep_fp64_probe.restype = i
+        lib.sweep_launch_floor.argtypes = [i, i, ctypes.POINTER(ctypes.c_double)]
+        lib.sweep_launch_floor.restype = i
         lib.sweep_nccl_unique_id.argtypes = [vp]
         lib.sweep_nccl_unique_id.restype = i
         lib.sweep_destroy.argtypes = [vp]
         lib.sweep_destroy.restype = None
         lib.sweep_last_error.argtypes = [vp]
         lib.sweep_last_error.restype = ctypes.c_char_p
+        lib._name_abs = os.path.abspath(path)
         _lib = lib
     return _lib
 
@@ -110,8 +119,37 @@ def fp64_probe(device: int = 0) -> float:
     return t.value
 
 
+def launch_floor(device: int = 0, reps: int = 2000) -> float:
+    """Device time per launch of an empty kernel, back to back on one stream (microseconds)."""
+    lib = load_library()
+    t = ctypes.c_double()
+    rc = lib.sweep_launch_floor(device, reps, ctypes.byref(t))
+    if rc:
+        raise SweepError(rc, lib.sweep_last_error(None).decode())
+    return t.value
+
+
 def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _check_dev(name: str, t, numel: int, device: int) -> None:
+    """A contiguous float64 CUDA tensor on `device` with exactly `numel` elements."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+    if t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the handle on cuda:{device}")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+
+
+def _check_host(name: str, a, numel: int) -> None:
+    """A C-contiguous float64 numpy array with exactly `numel` elements."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{name} must be a C-contiguous float64 numpy array")
+    if a.size != numel:
+        raise ValueError(f"{name} has {a.size} elements, expected {numel}")
 
 
 class Sweep:
@@ -147,6 +185,9 @@ class Sweep:
         self._check(self._lib.sweep_layout(self._h, off, ctypes.byref(tot)))
         self.offsets = list(off)
         self.out_size = tot.value
+        self.n = (p + 1) ** dim
+        self.n_el = nx * self.ny
+        self.n_bnode = 2 if dim == 1 else 2 * (nx + self.ny) * (p + 1)
 
     # ---------------------------------------------------------------- helpers
     def _check(self, rc: int):
@@ -163,9 +204,9 @@ class Sweep:
     # ---------------------------------------------------------------- ABI calls
     def sweep_run(self, sigma, inv_c_dt: float, q, inflow, stream=None) -> None:
         """sigma [N_el][G], q [N_el][n][G], inflow [N_bnode][G]: contiguous float64 CUDA tensors."""
-        for t in (sigma, q, inflow):
-            if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
-                raise ValueError("inputs must be contiguous float64 CUDA tensors")
+        _check_dev("sigma", sigma, self.n_el * self.G, self.device)
+        _check_dev("q", q, self.n_el * self.n * self.G, self.device)
+        _check_dev("inflow", inflow, self.n_bnode * self.G, self.device)
         self._check(self._lib.sweep_run(self._h, sigma.data_ptr(), float(inv_c_dt), q.data_ptr(),
                                         inflow.data_ptr(), self._stream_ptr(stream)))
 
@@ -174,9 +215,11 @@ class Sweep:
         import torch
         if out is None:
             out = torch.empty(self.out_size, dtype=torch.float64, device=f"cuda:{self.device}")
-        if out.numel() != self.out_size or not out.is_contiguous():
-            raise ValueError("out must be contiguous with out_size elements")
-        self._check(self._lib.closures_get(self._h, out.data_ptr(), self.out_size, self._stream_ptr(stream)))
+        if not isinstance(out, torch.Tensor) or out.dtype != torch.float64 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float64 tensor")
+        if out.is_cuda and out.device.index != self.device:
+            raise ValueError(f"out is on cuda:{out.device.index}, the handle on cuda:{self.device}")
+        self._check(self._lib.closures_get(self._h, out.data_ptr(), out.numel(), self._stream_ptr(stream)))
         return out
 
     def sweep_run_host(self, sigma: np.ndarray, inv_c_dt: float, q: np.ndarray, inflow: np.ndarray,
@@ -184,33 +227,50 @@ class Sweep:
         """End-to-end with host arrays (pinned numpy views of torch pinned tensors recommended)."""
         if out is None:
             out = np.empty(self.out_size)
+        _check_host("sigma", sigma, self.n_el * self.G)
+        _check_host("q", q, self.n_el * self.n * self.G)
+        _check_host("inflow", inflow, self.n_bnode * self.G)
+        if not isinstance(out, np.ndarray) or out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"] or \
+                not out.flags["WRITEABLE"]:
+            raise ValueError("out must be a writeable C-contiguous float64 numpy array")
         self._check(self._lib.sweep_run_host(self._h, sigma.ctypes.data, float(inv_c_dt), q.ctypes.data,
-                                             inflow.ctypes.data, out.ctypes.data, self.out_size,
+                                             inflow.ctypes.data, out.ctypes.data, out.size,
                                              self._stream_ptr(stream)))
         return out
 
     def trt_step(self, sigma, inflow, Tk, Iprev, nu, cv: float, dt: float, eps: float = 1e-4, max_iter: int = 50,
-                 T=None, stream=None):
+                 T=None, stream=None, return_ratios: bool = False):
         """One unaccelerated backward-Euler TRT step (include/sweep.h trt_step): CUDA float64
         tensors sigma [N_el][G], inflow [N_bnode][G], Tk [N_el][n], Iprev [N_el][n][G];
-        nu: host group bounds [G+1].  Returns (T tensor [N_el][n], outer iterations)."""
-        import torch
-        for t in (sigma, inflow, Tk, Iprev):
-            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-                raise ValueError("inputs must be contiguous float64 CUDA tensors")
+        nu: host group bounds [G+1].  Returns (T tensor [N_el][n], outer iterations) or, with
+        return_ratios, also ||u^l - u^(l-1)|| / ||u^1 - u^0|| per iteration (eq:relative_tol)."""
+        _check_dev("sigma", sigma, self.n_el * self.G, self.device)
+        _check_dev("inflow", inflow, self.n_bnode * self.G, self.device)
+        _check_dev("Tk", Tk, self.n_el * self.n, self.device)
+        _check_dev("Iprev", Iprev, self.n_el * self.n * self.G, self.device)
         if T is None:
+            import torch
             T = torch.empty_like(Tk)
-        nu_a = np.ascontiguousarray(nu, dtype=np.float64)
-        prm = trt_params(_dptr(nu_a), float(cv), float(dt), float(eps), int(max_iter))
+        _check_dev("T", T, self.n_el * self.n, self.device)
+        if int(max_iter) < 1:
+            raise ValueError("max_iter must be >= 1")
+        nu_a = np.ascontiguousarray(nu, dtype=np.float64).reshape(-1)
+        if nu_a.size != self.G + 1:
+            raise ValueError(f"nu has {nu_a.size} bounds, expected G + 1 = {self.G + 1}")
+        ratios = np.zeros(int(max_iter))
+        prm = trt_params(_dptr(nu_a), float(cv), float(dt), float(eps), int(max_iter), _dptr(ratios))
         it = ctypes.c_int()
         self._check(self._lib.trt_step(self._h, sigma.data_ptr(), inflow.data_ptr(), Tk.data_ptr(), Iprev.data_ptr(),
                                        ctypes.byref(prm), T.data_ptr(), ctypes.byref(it), self._stream_ptr(stream)))
+        if return_ratios:
+            return T, it.value, ratios[:it.value].copy()
         return T, it.value
 
     def stats(self) -> dict:
-        a = (ctypes.c_longlong * 4)()
+        a = (ctypes.c_longlong * 8)()
         self._check(self._lib.sweep_stats(self._h, a))
-        return {"launches": a[0], "directions_swept": a[1], "streams": a[2], "ctas": a[3]}
+        return {"launches": a[0], "directions_swept": a[1], "streams": a[2], "ctas": a[3], "block": a[4],
+                "groups_per_lane": a[5], "lanes_per_direction": a[6], "sms": a[7]}
 
     def timing(self, enable: bool = True) -> None:
         self._check(self._lib.sweep_timing(self._h, 1 if enable else 0))

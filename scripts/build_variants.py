@@ -1,4 +1,5 @@
-"""Experiment builds of libsweep.so with -D overrides, into build/<name>.so (used with SWEEP_LIB=...).
+"""Experiment builds of libsweep.so with -D overrides (plus -DSWEEP_EXPERIMENTS: the SWEEP_CFG /
+SWEEP_MAXWARPS layout overrides), into build/<name>.so (bench.py --lib build/<name>.so).
 usage: python scripts/build_variants.py name1:-DFOO=1,-DBAR name2: ..."""
 import os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -7,7 +8,7 @@ from paper_2504_21784_b200 import build as b
 os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
 def one(spec):
     name, _, defs = spec.partition(":")
-    flags = [d for d in defs.split(",") if d]
+    flags = ["-DSWEEP_EXPERIMENTS"] + [d for d in defs.split(",") if d]
     out = os.path.join(ROOT, "build", name + ".so")
     try:
         b.build(extra=flags, out=out)

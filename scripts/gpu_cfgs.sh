@@ -1,7 +1,7 @@
 # kernel time of configs C3, C4 and the C5 per-rank shards (G_loc = 8, 16) for build/<lib>.so variants
 for v in "$@"; do
   for c in 3 4; do
-    SWEEP_LIB=build/$v.so timeout 300 python bench.py --config $c --no-e2e --no-cpu --steps 20 > gpurun_out/cf_${v}_$c.json 2> gpurun_out/cf_${v}_$c.err
+    timeout 300 python bench.py --lib build/$v.so --config $c --no-e2e --no-cpu --steps 20 > gpurun_out/cf_${v}_$c.json 2> gpurun_out/cf_${v}_$c.err
     python -c "
 import json
 try:
@@ -9,5 +9,5 @@ try:
 except Exception as e: print('$v C$c ERR', open('gpurun_out/cf_${v}_$c.err').read()[-300:])
 "
   done
-  SWEEP_LIB=build/$v.so timeout 300 python scripts/shard_perf.py 8,16 "" 8 2>&1 | sed "s/^/$v /"
+  SWEEP_SHARD_LIB=build/$v.so timeout 300 python scripts/shard_perf.py 8,16 "" 8 2>&1 | sed "s/^/$v /"
 done

@@ -1,5 +1,5 @@
 for v in "$@"; do for c in 5 4 3; do
-SWEEP_LIB=build/$v.so timeout 120 python bench.py --config $c --no-e2e --no-cpu --steps 5 > gpurun_out/cx.json 2> gpurun_out/cx.err
+timeout 120 python bench.py --lib build/$v.so --config $c --no-e2e --no-cpu --steps 5 > gpurun_out/cx.json 2> gpurun_out/cx.err
 python -c "
 import json
 try:

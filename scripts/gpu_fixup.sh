@@ -1,7 +1,7 @@
 # time the C5 fixup option (kernel only) for build/<lib>.so under SWEEP_CFG layouts: args lib:cfg ...
 for spec in "$@"; do
   lib=${spec%%:*}; cfg=${spec#*:}; tag=${lib}_${cfg/,/x}
-  SWEEP_CFG=$cfg SWEEP_LIB=build/$lib.so timeout 300 python bench.py --no-e2e --no-cpu --steps 5 --opts fixup > gpurun_out/fx_$tag.json 2> gpurun_out/fx_$tag.err
+  SWEEP_CFG=$cfg timeout 300 python bench.py --lib build/$lib.so --no-e2e --no-cpu --steps 5 --opts fixup > gpurun_out/fx_$tag.json 2> gpurun_out/fx_$tag.err
   python -c "
 import json
 try:

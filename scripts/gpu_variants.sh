@@ -1,6 +1,6 @@
 # time bench.py (C5, kernel only) for each build/<name>.so given as args
 for v in "$@"; do
-  SWEEP_LIB=build/$v.so timeout 300 python bench.py --no-e2e --no-cpu --steps 5 > gpurun_out/var_$v.json 2> gpurun_out/var_$v.err
+  timeout 300 python bench.py --lib build/$v.so --no-e2e --no-cpu --steps 5 > gpurun_out/var_$v.json 2> gpurun_out/var_$v.err
   python -c "
 import json,sys
 try:

@@ -1,9 +1,11 @@
 """Per-rank workload of the group-sharded C5 run on one GPU (analysis only: one process,
-G_loc groups of C5), for every lane layout override given in SWEEP_CFG_LIST."""
+G_loc groups of C5), for every lane layout override given in SWEEP_CFG_LIST (needs an
+experiment build: scripts/build_variants.py, selected with SWEEP_SHARD_LIB=build/<name>.so)."""
 import os, sys, json
 import numpy as np, torch
 sys.path.insert(0, '.')
 import synth, paper_2504_21784_b200.sweep as S
+if os.environ.get("SWEEP_SHARD_LIB"): S.load_library(os.environ["SWEEP_SHARD_LIB"])
 prob = synth.config(5)
 dev = torch.device("cuda:0")
 for G in [int(x) for x in sys.argv[1].split(",")]:

@@ -1,12 +1,12 @@
 """Randomised GPU-vs-oracle parity sweep over shapes, orders, lane layouts and options
 (evidence beyond the pytest cases).  usage: python scripts/stress_parity.py N seed"""
-import sys, time
+import os, sys, time
 sys.path.insert(0, '.')
 import numpy as np
 import oracle, synth
 from synth.configs import random_problem
 import paper_2504_21784_b200 as pk
-from tests.parity import field_errors
+from tests.parity import field_errors, field_ok
 
 n, seed = int(sys.argv[1]), int(sys.argv[2])
 rng = np.random.default_rng(seed)
@@ -36,7 +36,7 @@ for i in range(n):
         e = field_errors(got, ref, dim, nx, ny, p, bool(opts & 1), bool(opts & 4))
         m = max(v[0] for v in e.values())
         worst = max(worst, m)
-        ok = all(v[0] <= (1e-11 if v[1] == "rel" else 1e-13) for v in e.values())
+        ok = all(field_ok(v) for v in e.values())
     except Exception as ex:  # noqa: BLE001
         ok, m = False, float("nan")
         print("EXC", ex)

@@ -7,6 +7,12 @@ import numpy as np
 TOL = 1e-11          # north_star: relative L-infinity error per output field, FP64
 TINY = 1e-8          # a field whose reference norm is below TINY * |phi| is compared absolutely
 ABS_TOL = 1e-13      # ... with |delta| <= ABS_TOL * |phi|
+# Cancellation quantities (reading R16): T = sum w (Omega Omega - I/3) psi and
+# beta = sum w (|Omega.n| - alpha) psi are weighted sums whose weights have both signs, with
+# |weight| <= w, so their rounding error is bounded by eps * sum w psi = eps * phi, not by eps
+# times their own (possibly much smaller) value.  Such a field passes if its relative error
+# is <= TOL, or its error is at the rounding level of phi: |delta| <= ABS_TOL * |phi|.
+CANCEL = ("Txx", "Txy", "Tyy", "beta")
 
 
 def fields(out: np.ndarray, dim: int, nx: int, ny: int, p: int, sigma_moments: bool = False,
@@ -53,15 +59,20 @@ def field_errors(got: np.ndarray, ref: np.ndarray, dim: int, nx: int, ny: int, p
             res[k] = (np.inf, "rel")
             continue
         nref = np.abs(fr[k]).max() if fr[k].size else 0.0
-        if nref >= TINY * base:
+        if nref >= TINY * base and not (k in CANCEL and d / nref > TOL and d <= ABS_TOL * base):
             res[k] = (d / nref, "rel")
         else:
             res[k] = (d / base, "abs_phi")
     return res
 
 
+def field_ok(err: tuple, tol: float = TOL) -> bool:
+    """One (error, kind) entry of field_errors against its bar."""
+    return err[0] <= (tol if err[1] == "rel" else ABS_TOL)
+
+
 def assert_parity(got, ref, dim, nx, ny, p, tol=TOL, sigma_moments=False, half_range=False):
     errs = field_errors(got, ref, dim, nx, ny, p, sigma_moments, half_range)
-    bad = {k: v for k, v in errs.items() if v[0] > (tol if v[1] == "rel" else ABS_TOL)}
+    bad = {k: v for k, v in errs.items() if not field_ok(v, tol)}
     assert not bad, f"parity failed: {bad} (all: {errs})"
     return errs

@@ -224,17 +224,16 @@ def test_host_api_matches_device_api(lib):
     assert np.array_equal(a, b)
 
 
-def test_nccl_allreduce_plumbing_one_rank(lib, monkeypatch):
+def test_nccl_allreduce_plumbing_one_rank(lib):
     """The NCCL path (dlopen of the libnccl torch loaded, ncclGetUniqueId, ncclCommInitRank,
     the in-place ncclAllReduce on the sweep's stream, ncclCommDestroy) on a 1-rank
-    communicator (SWEEP_FORCE_NCCL): the output equals the plain run bit for bit."""
+    communicator (flag SWEEP_FORCE_COMM): the output equals the plain run bit for bit."""
     import torch
     prob = synth.config(4, nx=24, G=6)
     plain = gpu_out(lib, prob)
-    monkeypatch.setenv("SWEEP_FORCE_NCCL", "1")
     nid = lib.nccl_unique_id()
     dev = torch.device("cuda:0")
-    with lib.from_problem(prob, nranks=1, rank=0, nccl_id=nid) as sw:
+    with lib.from_problem(prob, nranks=1, rank=0, nccl_id=nid, flags=lib.FORCE_COMM) as sw:
         s, q, f = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (prob.sigma, prob.q, prob.inflow))
         sw.timing(True)
         for _ in range(3):

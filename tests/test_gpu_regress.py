@@ -1,0 +1,161 @@
+"""GPU regression and self-consistency tests (-m gpu), through the C-ABI:
+
+* the two ill-conditioned cases an 8000-case random stress run of round 1 found just above
+  1e-11: the half-range P+ of a set whose only Omega_x >= 0 direction has
+  Omega_y^2 << 1/3, and beta of a 1-D set whose |mu| - alpha nearly cancel;
+* 90-degree rotation invariance at full C5 size (SURVEY §8c "Orientation"; the R7 product
+  set is symmetric under the rotation): the rotated problem's outputs are the
+  rotated outputs, a check of the quadrant mirroring that needs no oracle;
+* bench.py end to end on config C4 (the contract JSON line, with roofline, e2e, clocks).
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth.configs import Problem, random_problem
+from tests.parity import assert_parity, field_errors
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device on a -m gpu run")
+    from paper_2504_21784_b200 import build
+    build.build()
+    import paper_2504_21784_b200 as pk
+    pk.load_library()
+    return pk
+
+
+# ------------------------------------------------------------------ stress regressions
+def _unit(ox, oy):
+    oz2 = 1.0 - ox * ox - oy * oy
+    return [ox, oy, np.sqrt(oz2)]
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_halfrange_P_small_omega_y(pk, p):
+    """P+_{+x, yy} = sum_{Omega_x >= 0} w Omega_y^2 psi with the only Omega_x >= 0 direction at
+    Omega_y = 0.004: formed as T + phi/3 it cancels to ~1e-5 of its terms; the untraced rows
+    the sweep now writes keep it at full relative accuracy."""
+    om = np.array([_unit(0.6, 0.004), _unit(-0.5, 0.7), _unit(-0.3, -0.8)])
+    w = np.array([0.3, 0.45, 0.25])
+    prob = random_problem(91_001, 2, 7, 5, p, 3, 5, omega=om, w=w)
+    ref = oracle.sweep(prob, opts=oracle.HALF_RANGE)
+    got = pk.run_problem(prob, flags=pk.HALF_RANGE)
+    errs = assert_parity(got, ref, 2, prob.nx, prob.ny, p, half_range=True)
+    assert errs["P+x_yy"][1] == "rel" and errs["P+x_yy"][0] <= 1e-11
+
+
+@pytest.mark.parametrize("half", [False, True])
+def test_halfrange_1d_small_mu(pk, half):
+    """1-D P+ with the only mu > 0 direction at mu = 0.01 (P = T + phi/3 cancellation)."""
+    om = np.array([[0.01, 0, 0], [-0.7, 0, 0], [-0.2, 0, 0]])
+    w = np.array([0.5, 0.3, 0.2])
+    prob = random_problem(91_002, 1, 40, 1, 1, 3, 4, omega=om, w=w)
+    flags = pk.HALF_RANGE if half else 0
+    ref = oracle.sweep(prob, opts=oracle.HALF_RANGE if half else 0)
+    got = pk.run_problem(prob, flags=flags)
+    assert_parity(got, ref, 1, prob.nx, 1, 1, half_range=half)
+
+
+def test_beta_1d_cancelling_weights(pk):
+    """beta = sum w (|mu| - alpha) psi with |mu_1| = |mu_2| + 1e-7: every weight is ~1e-7 of w,
+    so beta is a cancellation quantity (reading R16): passes relative to itself or at the
+    rounding level of phi."""
+    om = np.array([[0.55, 0, 0], [-0.5500001, 0, 0]])
+    w = np.array([0.5, 0.5])
+    for seed, p in ((91_003, 1), (91_004, 2)):
+        prob = random_problem(seed, 1, 64, 1, p, 2, 8, omega=om, w=w)
+        ref = oracle.sweep(prob)
+        got = pk.run_problem(prob)
+        errs = assert_parity(got, ref, 1, prob.nx, 1, p)
+        phi = np.abs(ref[:prob.n_el * prob.n]).max()
+        beta = got[prob.n_el * prob.n * 3:prob.n_el * prob.n * 3 + 2]
+        beta_ref = ref[prob.n_el * prob.n * 3:prob.n_el * prob.n * 3 + 2]
+        assert np.abs(beta - beta_ref).max() <= 1e-13 * phi, errs["beta"]
+
+
+# ------------------------------------------------------------------ 90-degree rotation at C5 size
+def _rotation_maps(N: int, p: int):
+    """Index maps of the counter-clockwise rotation (x, y) -> (1 - y, x) on an N x N mesh:
+    element (i, j) -> (N-1-j, i), node (a, b) -> (p-b, a); faces x- -> y-, y- -> x+,
+    x+ -> y+, y+ -> x-.  Returns (node_src, bnode_src): for every node / boundary face node of
+    the ROTATED problem, the index of the original node / boundary node it comes from."""
+    np1 = p + 1
+    n = np1 * np1
+    e_src = np.empty(N * N, dtype=np.int64)
+    k_src = np.empty(n, dtype=np.int64)
+    for i in range(N):
+        for j in range(N):
+            e_src[(N - 1 - j) + N * i] = i + N * j
+    for a in range(np1):
+        for b in range(np1):
+            k_src[(p - b) + np1 * a] = a + np1 * b
+    node_src = (e_src[:, None] * n + k_src[None, :]).ravel()
+
+    def bidx(face, idx, node):
+        return [0, N * np1, 2 * N * np1, 3 * N * np1][face] + idx * np1 + node
+
+    bn_src = np.empty(4 * N * np1, dtype=np.int64)
+    for idx in range(N):
+        for t in range(np1):
+            bn_src[bidx(2, N - 1 - idx, p - t)] = bidx(0, idx, t)    # x- (j=idx, b=t) -> y- (i'=N-1-j, a'=p-b)
+            bn_src[bidx(1, idx, t)] = bidx(2, idx, t)                # y- (i=idx, a=t) -> x+ (j'=i, b'=a)
+            bn_src[bidx(3, N - 1 - idx, p - t)] = bidx(1, idx, t)    # x+ (j=idx, b=t) -> y+ (i'=N-1-j, a'=p-b)
+            bn_src[bidx(0, idx, t)] = bidx(3, idx, t)                # y+ (i=idx, a=t) -> x- (j'=i, b'=a)
+    return e_src, node_src, bn_src
+
+
+def test_rotation_invariance_c5(pk):
+    prob = synth.config(5)
+    N, p, n = prob.nx, prob.p, prob.n
+    e_src, node_src, bn_src = _rotation_maps(N, p)
+    rot = Problem("C5rot", 2, N, N, p, prob.omega, prob.w, prob.sigma[e_src],
+                  prob.q.reshape(-1, prob.G)[node_src].reshape(prob.q.shape), prob.inflow[bn_src], prob.inv_c_dt)
+    a = pk.run_problem(prob)
+    b = pk.run_problem(rot)
+    nodes = prob.n_el * n
+    f = lambda o, r: o[r * nodes:(r + 1) * nodes]  # noqa: E731
+    nb = prob.n_bnode
+    # expected outputs of the rotated problem from the original ones
+    exp = np.empty_like(a)
+    exp[0:nodes] = f(a, 0)[node_src]                        # phi
+    exp[nodes:2 * nodes] = -f(a, 2)[node_src]               # J'_x = -J_y
+    exp[2 * nodes:3 * nodes] = f(a, 1)[node_src]            # J'_y = J_x
+    exp[3 * nodes:4 * nodes] = f(a, 5)[node_src]            # T'_xx = T_yy
+    exp[4 * nodes:5 * nodes] = -f(a, 4)[node_src]           # T'_xy = -T_xy
+    exp[5 * nodes:6 * nodes] = f(a, 3)[node_src]            # T'_yy = T_xx
+    exp[6 * nodes:6 * nodes + nb] = a[6 * nodes:6 * nodes + nb][bn_src]               # beta
+    exp[6 * nodes + nb:6 * nodes + 2 * nb] = a[6 * nodes + nb:6 * nodes + 2 * nb][bn_src]  # J+
+    errs = field_errors(b, exp, 2, N, N, p)
+    assert max(e for e, _ in errs.values()) <= 1e-12, errs
+
+
+# ------------------------------------------------------------------ bench end to end
+def test_bench_config4_contract():
+    r = subprocess.run([sys.executable, "bench.py", "--config", "4", "--steps", "3", "--warmup", "3", "--no-cpu"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 3 and d["dtype"] == "f64" and d["gpu_launches"] > 0
+    assert d["config"]["workload"].startswith("C4")
+    assert 0 < d["roofline"]["frac"] < 1 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["parity"]["max_error"] <= 1e-11

@@ -250,15 +250,61 @@ def _trt_problem(dim, p, nx, ny, G, seed=5):
 
 
 def test_trt_step_equilibrium():
-    """Uniform equilibrium (T = T0 everywhere, I^k = inflow = B_g(T0)) is a fixed point:
-    one iteration, T = T0."""
+    """Uniform equilibrium (T = T0 everywhere, I^k = inflow = B_g(T0)) is a fixed point: T
+    stays T0.  u^1 - u^0 is rounding noise, so eq:relative_tol (relative to it) either stops
+    at once (exactly zero) or runs to max_iter; T = T0 either way."""
     prob, Tk, Iprev, nu = _trt_problem(2, 1, 3, 3, 4)
     T0 = 0.8
     Tk[:] = T0
     Iprev[:] = oracle.planck_groups(T0, nu)
     prob.inflow[:] = oracle.planck_groups(T0, nu)
     T, it = oracle.trt_step(prob, Tk, Iprev, nu, cv=0.3, dt=0.05, eps=1e-12, max_iter=5)
-    assert np.abs(T - T0).max() < 1e-13 and it == 1
+    assert np.abs(T - T0).max() < 1e-13 and it in (1, 5)
+
+
+@pytest.mark.parametrize("dim,p,eps", [(1, 1, 1e-4), (2, 1, 1e-4), (2, 2, 1e-3), (1, 2, 3e-2)])
+def test_trt_stop_rule_rebuilt(dim, p, eps):
+    """Pin of the outer stopping rule (eq:relative_tol, eps = 1e-4 for the
+    unaccelerated scheme PAPER.md:669): rebuild the iterate sequence u^l = [T^l, E^l] from
+    fixed-iteration runs (T^l = the l-iteration step, E^l = phi of the sweep on the emission
+    of T^(l-1), E^0 = sum_g I^k_g), find the first l >= 2 with ||u^l - u^(l-1)||_2 <
+    eps ||u^1 - u^0||_2 here, and require the oracle to stop exactly there with T = T^l."""
+    nx, ny, G = (6, 1, 3) if dim == 1 else (3, 3, 3)
+    prob, Tk, Iprev, nu = _trt_problem(dim, p, nx, ny, G, seed=11)
+    cv, dt = 0.1, 0.05
+    ne, n = Tk.shape
+    u_prev = np.concatenate([Tk.ravel(), Iprev.sum(axis=-1).ravel()])
+    T_prev = Tk
+    norms, Ts = [], []
+    for l in range(1, 60):
+        T_l, it_l = oracle.trt_step(prob, Tk, Iprev, nu, cv=cv, dt=dt, eps=0.0, max_iter=l)
+        assert it_l == l
+        q = np.zeros((ne, n, G))
+        for e in range(ne):
+            for k in range(n):
+                q[e, k] = prob.sigma[e] * oracle.planck_groups(T_prev[e, k], nu) + Iprev[e, k] / dt
+        pr = Problem("rb", prob.dim, prob.nx, prob.ny, p, prob.omega, prob.w, prob.sigma, q, prob.inflow, 1.0 / dt)
+        E_l = oracle.sweep(pr)[:ne * n]
+        u_l = np.concatenate([T_l.ravel(), E_l])
+        norms.append(np.linalg.norm(u_l - u_prev))
+        Ts.append(T_l)
+        u_prev, T_prev = u_l, T_l
+        if l >= 2 and norms[-1] < eps * norms[0]:
+            break
+    else:
+        pytest.fail("sequence did not meet the tolerance in 59 iterations")
+    want = len(norms)
+    assert want >= 3   # the case exercises more than the first comparison
+    T, it, ratios = oracle.trt_step(prob, Tk, Iprev, nu, cv=cv, dt=dt, eps=eps, max_iter=100, return_ratios=True)
+    assert it == want
+    assert np.array_equal(T, Ts[-1])
+    np.testing.assert_allclose(ratios, np.array(norms) / norms[0], rtol=1e-12, atol=0)
+    # a tolerance just above the second-to-last ratio stops one iteration earlier (if that
+    # is still an iteration >= 2), just below it does not
+    if want >= 4:
+        _, it_hi = oracle.trt_step(prob, Tk, Iprev, nu, cv=cv, dt=dt, eps=ratios[-2] * (1 + 1e-9), max_iter=100)
+        _, it_lo = oracle.trt_step(prob, Tk, Iprev, nu, cv=cv, dt=dt, eps=ratios[-2] * (1 - 1e-9), max_iter=100)
+        assert it_hi == want - 1 and it_lo == want
 
 
 @pytest.mark.parametrize("dim,p", [(1, 1), (2, 1)])
