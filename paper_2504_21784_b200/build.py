@@ -9,6 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsweep.so")
+# debug build: device-side bounds checks and trace-ring tags (-DSWEEP_DEBUG), same ABI
+DEBUG_LIB = os.path.join(HERE, "libsweep_debug.so")
 # device code is split over translation units that compile in parallel
 # (k2d_*.cu instantiate the 2-D kernel templates of sweep_device.cuh)
 SOURCES = [os.path.join(CSRC, f) for f in ("k2d_p2.cu", "k2d_opt_p2.cu", "k2d_p1.cu", "k2d_opt_p1.cu",
@@ -27,10 +29,10 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
@@ -59,6 +61,13 @@ def link(objs: list, out: str) -> None:
     subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-ldl"])
 
 
+def build_debug(force: bool = False) -> str:
+    """libsweep_debug.so: the same library with -DSWEEP_DEBUG (tests/test_gpu_debug.py)."""
+    if not force and not stale(DEBUG_LIB):
+        return DEBUG_LIB
+    return build(force=True, extra=("-DSWEEP_DEBUG",), out=DEBUG_LIB)
+
+
 def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) -> str:
     if out == LIB and not extra and not force and not stale():
         return LIB
@@ -76,3 +85,5 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)
+    if "--debug" in sys.argv:
+        print(build_debug(force="--force" in sys.argv))

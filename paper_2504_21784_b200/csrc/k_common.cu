@@ -202,9 +202,14 @@ int sweep2d_cols_per_chunk(int p, int k, int opt) { return cols_per_chunk(p, k, 
 // value set by a later handle would make an earlier handle's larger launch fail).
 static int raise_smem_cap(const void* f) {
     int dev = 0, optin = 0;
+    cudaFuncAttributes fa;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+    // opt-in maximum minus the kernel's static shared memory
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) (void)cudaGetLastError();  // do not leave the error pending for a later launch check
     return (int)e;
 }
 
@@ -304,6 +309,12 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters
     const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
     if (r == 1.2345) sink[threadIdx.x] = r;  // keep the chains alive
 }
+
+#ifdef SWEEP_DEBUG
+int debug_build() { return 1; }
+#else
+int debug_build() { return 0; }
+#endif
 
 // empty-kernel launch floor: reps back-to-back launches of an empty kernel on one stream,
 // timed with events on that stream (device-side time per launch, host enqueue overlapped)

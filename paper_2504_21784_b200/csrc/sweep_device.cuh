@@ -46,6 +46,21 @@ namespace sweepk {
 
 static __constant__ ModalConsts cM;  // per translation unit
 
+// Debug builds (-DSWEEP_DEBUG, libsweep_debug.so): every global index is bounds-checked and
+// every strip-boundary trace read checks the ring slot's tag (written by the strip below);
+// a failed check sets bit 32 of the device error flag (reported by closures_get) instead of
+// faulting, so the CUDA context survives.  Release builds compile the checks away.
+#ifdef SWEEP_DEBUG
+#define SWEEP_DCHECK(cond)                  \
+    do {                                    \
+        if (!(cond)) atomicOr(prm.err, 32); \
+    } while (0)
+#else
+#define SWEEP_DCHECK(cond) \
+    do {                   \
+    } while (0)
+#endif
+
 #ifdef SWEEP_TRACE
 // debug timeline (trace builds only): per task [start, end, waited ns, sm id]
 static __device__ long long g_trace[1 << 18][8];
@@ -598,6 +613,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         const int ip = i0s + col, jp = j0 + r;
                         const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
                         const size_t e = (size_t)i + (size_t)nx * j;
+                        SWEEP_DCHECK(i >= 0 && i < nx && j >= 0 && j < ny && sd.g0 + sd.ng <= G);
                         if (kk < NN)
                             bulk_g2s_hint(qd + ((size_t)el * NN + kk) * GBK, prm.q + (e * NN + kk) * G + sd.g0,
                                           row_bytes, &mbar[b], pol_first);
@@ -617,6 +633,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         const int ip = i0s + col, jp = j0 + r;
                         const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
                         const size_t e = (size_t)i + (size_t)nx * j;
+                        SWEEP_DCHECK(i >= 0 && i < nx && j >= 0 && j < ny && sd.g0 + gg < G);
                         if (kk < NN)
                             cp_async8(qd + ((size_t)el * NN + kk) * GBK + gg, prm.q + (e * NN + kk) * G + sd.g0 + gg, 8);
                         else
@@ -691,6 +708,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                     for (int bq = 0; bq < NP1; ++bq) {
                         const int b = fy ? P - bq : bq;
+                        SWEEP_DCHECK(bnode2d(fx ? 1 : 0, j, b, nx, ny, NP1) < prm.nbnode && g < G);
                         t[bq] = prm.inflow[(size_t)bnode2d(fx ? 1 : 0, j, b, nx, ny, NP1) * G + g];
                     }
                 }
@@ -759,6 +777,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             const int ip = i0 + col, jp = j0 + r;
                             const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
                             double* dst = field_dst(f) + ((size_t)i + (size_t)nx * j) * NN;
+                            SWEEP_DCHECK(dst + NN <= prm.slabs + ((size_t)s + 1) * prm.out_size && i >= 0 && i < nx &&
+                                         j >= 0 && j < ny);
                             // p = 2: the slab keeps the MODAL values (sweep orientation); the
                             // finalize kernel applies each stream's back transform once per
                             // output instead of every CTA per chunk.  p = 1: nodal already.
@@ -813,6 +833,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             vj = Mj[kk];
                         }
                         const int bn = bnode2d(face, idx, t, nx, ny, NP1);
+                        SWEEP_DCHECK(bn >= 0 && bn < prm.nbnode);
                         slab[6 * nodes + bn] = vb;
                         slab[6 * nodes + prm.nbnode + bn] = vj;
                     }
@@ -895,6 +916,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             if (false) {
 #endif
                 const int* f = prm.progress + (size_t)s * prm.n_strips + (J - 1);
+                SWEEP_DCHECK(s < prm.n_streams && J - 1 < prm.n_strips);
                 // watchdog: a predecessor that never arrives (a bug) must not hang the GPU
                 const long long t_start = clock64();
 #ifdef SWEEP_TRACE
@@ -970,6 +992,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                         for (int aq = 0; aq < NP1; ++aq) {
                             const int a = fx ? P - aq : aq;
+                            SWEEP_DCHECK(!on || (bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) < prm.nbnode && sd.g0 + gl < G));
                             t[aq] = on ? prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + sd.g0 + gl] : 0.0;
                         }
                         if constexpr (P == 2) {
@@ -982,6 +1005,12 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         }
                     }
                 } else {
+#ifdef SWEEP_DEBUG
+                    for (int col = 0; col < C; ++col) {
+                        SWEEP_DCHECK(ysrc + (size_t)(i0 + col + 1) * NT * NL <= prm.ytr + prm.ring_len);
+                        SWEEP_DCHECK(__ldcg(prm.ytag + ((size_t)s * 2 + ((J + 1) & 1)) * nxp + i0 + col) == J - 1);
+                    }
+#endif
 #pragma unroll
                     for (int col = 0; col < C; ++col)
 #pragma unroll
@@ -1032,6 +1061,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                         for (int t = 0; t < NT; ++t)
                             st_hint(ydst + (size_t)(i0 + col) * NT * NL + t * NL + tid, tyc[col][t], pol_last);
+#ifdef SWEEP_DEBUG
+                    SWEEP_DCHECK(ydst + (size_t)(i0 + C) * NT * NL <= prm.ytr + prm.ring_len);
+                    if (tid == 0)
+                        for (int col = 0; col < C; ++col) __stcg(prm.ytag + ((size_t)s * 2 + (J & 1)) * nxp + i0 + col, J);
+#endif
                 }
             } else
 #pragma unroll kColUnroll
@@ -1106,6 +1140,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     // this lane's traces of column ip: column 0 of a chunk straight from L2
                     // (issued after this chunk's acquire), later columns from the private
                     // shared-memory slots the previous column prefetched with cp.async
+#ifdef SWEEP_DEBUG
+                    SWEEP_DCHECK(ysrc + ((size_t)ip + 1) * K * NT * NL <= prm.ytr + prm.ring_len);
+                    SWEEP_DCHECK(__ldcg(prm.ytag + ((size_t)s * 2 + ((J + 1) & 1)) * nxp + ip) == J - 1);
+#endif
                     if (col == 0) {
 #pragma unroll
                         for (int k = 0; k < K; ++k)
@@ -1192,6 +1230,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                         for (int t = 0; t < NT; ++t)
                             st_hint(ydst + ((size_t)ip * K + k) * NT * NL + t * NL + tid, ty[k][t], pol_last);
+#ifdef SWEEP_DEBUG
+                    SWEEP_DCHECK(ydst + ((size_t)ip + 1) * K * NT * NL <= prm.ytr + prm.ring_len);
+                    if (tid == 0) __stcg(prm.ytag + ((size_t)s * 2 + (J & 1)) * nxp + ip, J);
+#endif
                 }
             }
             // this buffer is refilled by the async proxy two chunks from now
@@ -1315,6 +1357,7 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
 #pragma unroll
         for (int a = 0; a < NP1; ++a) q[a] = 0.0;
         if (g_on) {
+            SWEEP_DCHECK(i >= 0 && i < nx && g < G);
             sg = prm.sigma[(size_t)i * G + g];
             st = sg + prm.inv_c_dt;
             if (bad_sigma(st)) atomicOr(prm.err, 1);
@@ -1390,6 +1433,7 @@ __global__ void __launch_bounds__(1024) sweep1d_kernel(const Sweep1DParams prm) 
                 const size_t base = (m < 3)    ? (size_t)m * nodes
                                     : (m < NM) ? sig_off + (size_t)(m - 3) * nodes
                                                : prm.hr_off;
+                SWEEP_DCHECK(base + (size_t)(i + 1) * NP1 <= prm.out_size && i >= 0 && i < nx);
                 slab[base + (size_t)i * NP1 + a] = val;
             }
         };

@@ -113,6 +113,8 @@ struct sweep_handle {
     StreamDesc* d_streams = nullptr;
     int* d_progress = nullptr;  // [n_streams*n_strips] + task counter + err flag
     double* d_ytr = nullptr;
+    size_t ring_len = 0;
+    int* d_ytag = nullptr;  // debug builds: trace-ring tags
     double* d_slabs = nullptr;
     double* d_out = nullptr;
     int* d_err = nullptr;
@@ -525,6 +527,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         return fail(nullptr, SWEEP_E_CUDA, m);
     }
     auto bail = [&](int code) {
+        (void)cudaGetLastError();  // a failed setup leaves no pending error for later launch checks
         g_setup_error = h->err;
         sweep_destroy(h);
         return code;
@@ -573,8 +576,16 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->grid = std::min(h->n_tasks, bps * h->n_sm);
         const int NT = h->np1;
         h->progress_ints = (size_t)h->n_streams * h->n_strips;
-        if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * (size_t)h->n_streams * 2 * (h->n_chunks * C) * h->kpl * NT * h->block)))
+        h->ring_len = (size_t)h->n_streams * 2 * (h->n_chunks * C) * h->kpl * NT * h->block;
+        if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * h->ring_len)))
             return cuda_fail(h, ce, "cudaMalloc ytr"), bail(SWEEP_E_CUDA);
+        if (sweepk::debug_build()) {
+            const size_t ntag = (size_t)h->n_streams * 2 * (h->n_chunks * C);
+            if ((ce = cudaMalloc(&h->d_ytag, sizeof(int) * ntag)))
+                return cuda_fail(h, ce, "cudaMalloc ytag"), bail(SWEEP_E_CUDA);
+            if ((ce = cudaMemset(h->d_ytag, 0xff, sizeof(int) * ntag)))
+                return cuda_fail(h, ce, "memset ytag"), bail(SWEEP_E_CUDA);
+        }
     } else {
         // segmented affine scan of the chain; the fixup is not affine: one segment
         h->nseg = (h->opt & sweepk::OPT_FIXUP) ? 1 : std::min(32, std::max(1, (h->nx + 15) / 16));
@@ -646,6 +657,11 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
     // reset progress flags and the task counter (the error flag is sticky until closures_get)
     if ((ce = cudaMemsetAsync(h->d_progress, 0, sizeof(int) * (h->progress_ints + 1), st)))
         return cuda_fail(h, ce, "memset flags");
+    if (h->d_ytag &&  // debug builds: tags of this run only
+        (ce = cudaMemsetAsync(h->d_ytag, 0xff, sizeof(int) * (size_t)h->n_streams * 2 *
+                                                   (h->n_chunks * sweepk::sweep2d_cols_per_chunk(h->p, h->kpl, h->opt)),
+                              st)))
+        return cuda_fail(h, ce, "memset ytag");
     int e;
     h->launches = 0;
     cudaEvent_t* evs = nullptr;
@@ -684,6 +700,8 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.progress = h->d_progress;
         prm.task_counter = h->d_counter;
         prm.ytr = h->d_ytr;
+        prm.ring_len = h->ring_len;
+        prm.ytag = h->d_ytag;
         prm.slabs = h->d_slabs;
         prm.out_size = h->out_size;
         prm.nodes = h->nodes;
@@ -814,7 +832,8 @@ extern "C" int closures_get(sweep_handle* h, double* out, size_t n, void* stream
     if (flag) {
         cudaMemset(h->d_err, 0, sizeof(int));
         return fail(h, SWEEP_E_SIGMA,
-                    (flag & 4)   ? "internal: wavefront dependency timeout"
+                    (flag & 32)  ? "debug check failed: out-of-bounds index or trace-ring inconsistency"
+                    : (flag & 4) ? "internal: wavefront dependency timeout"
                     : (flag & 1) ? "sigma_t + 1/(c dt) <= 0 or non-finite sigma"
                                  : "non-finite result (non-finite q or inflow)");
     }
@@ -945,6 +964,7 @@ extern "C" void sweep_destroy(sweep_handle* h) {
     cudaFree(h->d_trt_E);
     cudaFree(h->d_progress);
     cudaFree(h->d_ytr);
+    cudaFree(h->d_ytag);
     cudaFree(h->d_slabs);
     cudaFree(h->d_out);
     cudaFree(h->d_in_sigma);

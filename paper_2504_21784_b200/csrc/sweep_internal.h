@@ -67,6 +67,8 @@ struct Sweep2DParams {
     int* progress;                 // [n_streams][n_strips] chunks completed
     int* task_counter;
     double* ytr;                   // [n_streams][2][nx][K][NT][NL]
+    size_t ring_len;               // doubles in ytr
+    int* ytag;                     // debug builds: [n_streams][2][nx_pad] strip that wrote the ring column
     double* slabs;                 // [n_streams][out_size]
     size_t out_size;
     size_t nodes;                  // N_el * n
@@ -112,6 +114,7 @@ int sweep2d_cols_per_chunk(int p, int k, int opt);
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
 int launch_floor(int device, int reps, double* us);
+int debug_build();  // 1 in -DSWEEP_DEBUG builds (bounds checks + trace-ring tags)
 
 // unaccelerated TRT iteration (k_trt.cu)
 int trt_blocks(int n_sm);
