@@ -17,6 +17,41 @@ __global__ void finalize_kernel(const double* __restrict__ slabs, int n_slabs, s
     if (bad) atomicOr(err, 2);
 }
 
+// many slabs (the 1-D scan writes one per CTA): a block of 32 outputs x 8 parts; part k sums
+// slabs [k n/8, (k+1) n/8) in order for its output (coalesced over the 32 outputs, 4 loads in
+// flight), then part 0 adds the 8 partials in order: a fixed summation tree (deterministic)
+__global__ void __launch_bounds__(256) finalize_many_kernel(const double* __restrict__ slabs, int n_slabs, size_t stride,
+                                                            size_t n, double* __restrict__ out, int* err) {
+    __shared__ double part[8][33];
+    const int lo = threadIdx.x & 31, k = threadIdx.x >> 5;
+    const int s0 = (int)((long long)n_slabs * k / 8), s1 = (int)((long long)n_slabs * (k + 1) / 8);
+    bool bad = false;
+    for (size_t base = (size_t)blockIdx.x * 32; base < n; base += (size_t)gridDim.x * 32) {
+        const size_t i = base + lo;
+        double acc = 0.0;
+        if (i < n) {
+            int s = s0;
+            for (; s + 4 <= s1; s += 4) {
+                const double a0 = __ldcs(slabs + (size_t)s * stride + i), a1 = __ldcs(slabs + (size_t)(s + 1) * stride + i),
+                             a2 = __ldcs(slabs + (size_t)(s + 2) * stride + i), a3 = __ldcs(slabs + (size_t)(s + 3) * stride + i);
+                acc = (((acc + a0) + a1) + a2) + a3;
+            }
+            for (; s < s1; ++s) acc += __ldcs(slabs + (size_t)s * stride + i);
+        }
+        part[k][lo] = acc;
+        __syncthreads();
+        if (k == 0 && i < n) {
+            double t = part[0][lo];
+#pragma unroll
+            for (int kk = 1; kk < 8; ++kk) t += part[kk][lo];
+            out[i] = t;
+            bad |= !(fabs(t) < 1.0e300);
+        }
+        __syncthreads();
+    }
+    if (bad) atomicOr(err, 2);
+}
+
 // ------------------------------------------------------------------ modal slabs (2-D, p = 2)
 // The p = 2 sweep kernel leaves its node fields in the slabs as MODAL values in its
 // stream's sweep orientation (physical element, 9 modal reals).  Physical node
@@ -178,6 +213,7 @@ int upload_modal(const ModalConsts& mc) {
     if (!e) e = upload_modal_p2(mc);
     if (!e) e = upload_modal_opt_p1(mc);
     if (!e) e = upload_modal_opt_p2(mc);
+    if (!e) e = upload_modal_1d(mc);
     return e;
 }
 
@@ -254,6 +290,8 @@ int reduce_caps(int n_sm, ReduceCaps* caps) {
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, finalize_modal_kernel, block, 0);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, halfrange_kernel, block, 0);
     if (e != cudaSuccess) return (int)e;
+    int d = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d, finalize_many_kernel, block, 0) == cudaSuccess && d < a) a = d;
     caps->finalize = n_sm * (a > 0 ? a : 1);
     caps->finalize_modal = n_sm * (b > 0 ? b : 1);
     caps->halfrange = n_sm * (c > 0 ? c : 1);
@@ -263,6 +301,11 @@ int reduce_caps(int n_sm, ReduceCaps* caps) {
 int launch_finalize(const double* slabs, int n_slabs, size_t stride, size_t n, double* out, int* err, int cap,
                     void* stream) {
     const int block = 256;
+    if (n_slabs > 8) {
+        const int grid = capped_grid((n + 31) / 32, cap);
+        finalize_many_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, n, out, err);
+        return (int)cudaGetLastError();
+    }
     const int grid = capped_grid((n + block - 1) / block, cap);
     finalize_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(slabs, n_slabs, stride, n, out, err);
     return (int)cudaGetLastError();

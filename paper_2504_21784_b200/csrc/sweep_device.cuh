@@ -659,7 +659,6 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         // SWEEP_HALF_RANGE: + the untraced P_xx, P_yy = sum w Omega_x^2 psi, sum w Omega_y^2 psi of
         // this stream (quadrant), into the stream slab's half-range rows (read by halfrange_kernel;
         // forming them as T + phi/3 there cancels when Omega^2 << 1/3)
-        const int nfo = NFO + (prm.half ? 2 : 0);
         double* bckS = ypre + K * NT * NL;     // [9][9] modal -> nodal (p = 2, boundary closures)
         double* S2 = bckS + 81;                // SIG: [CT][SEL] sigma-weighted group sums
 #ifndef SWEEP_DEFER_C
@@ -749,15 +748,59 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #define SWEEP_PC 1  // 4 (0.3 % faster at C5) hits an illegal-instruction fault in the p = 2, 2-lane layout with modal slabs
 #endif
                 constexpr int PC = SWEEP_PC;
-                for (int o0 = tid; o0 < CT * nfo * NQ; o0 += PC * NL) {
+                // NF node fields (compile time: the index arithmetic by constants); + 2 with
+                // SWEEP_HALF_RANGE
+                auto node_fields = [&](auto nf_c) {
+                constexpr int NF = decltype(nf_c)::value;
+#ifndef SWEEP_PC_TILED
+#define SWEEP_PC_TILED 1
+#endif
+                if constexpr (SWEEP_PC_TILED) {
+                    // one (element, mode) per thread and pass, ALL NF fields: one S load (two
+                    // with SIG) per direction feeds NF FMAs; the weights are warp-broadcast loads
+                    // (1.2 shared loads per FMA instead of 2)
+                    for (int o = tid; o < CT * NQ; o += NL) {
+                        const int m = o % NQ, el = o / NQ;
+                        const double* Sp = S + (size_t)el * SEL + m;
+                        const double* Sp2 = S2 + (size_t)el * SEL + m;
+                        double acc[NF];
+#pragma unroll
+                        for (int f = 0; f < NF; ++f) acc[f] = 0.0;
+                        for (int dd = 0; dd < sd.nd; ++dd) {
+                            const double sv = Sp[dd * NQ];
+                            const double sv2 = SIG ? Sp2[dd * NQ] : 0.0;
+                            const double* cf = coefS + dd * NFIELD;
+#pragma unroll
+                            for (int f = 0; f < NF; ++f) {
+                                const int ci = (f < 6) ? f : (f < NFO) ? f - 6 : 14 + (f - NFO);
+                                acc[f] = fma(cf[ci], (f >= 6 && f < NFO) ? sv2 : sv, acc[f]);
+                            }
+                        }
+                        const int col = el / T, r = el - col * T;
+                        if (col < cols && r < rows) {
+                            const int ip = i0 + col, jp = j0 + r;
+                            const int i = fx ? nx - 1 - ip : ip, j = fy ? ny - 1 - jp : jp;
+                            const size_t eo = ((size_t)i + (size_t)nx * j) * NN;
+#pragma unroll
+                            for (int f = 0; f < NF; ++f) {
+                                double* dst = field_dst(f) + eo;
+                                SWEEP_DCHECK(dst + NN <= prm.slabs + ((size_t)s + 1) * prm.out_size && i >= 0 &&
+                                             i < nx && j >= 0 && j < ny);
+                                if constexpr (P == 2) dst[m] = acc[f];
+                                else node_store(dst, m, acc[f]);
+                            }
+                        }
+                    }
+                } else {
+                for (int o0 = tid; o0 < CT * NF * NQ; o0 += PC * NL) {
                     const double* Sp[PC];
                     const double* cf[PC];
                     double acc[PC];
 #pragma unroll
                     for (int u = 0; u < PC; ++u) {
-                        const int o = min(o0 + u * NL, CT * nfo * NQ - 1);
+                        const int o = min(o0 + u * NL, CT * NF * NQ - 1);
                         const int m = o % NQ, rest = o / NQ;
-                        const int f = rest % nfo, el = rest / nfo;
+                        const int f = rest % NF, el = rest / NF;
                         Sp[u] = ((f < 6 || f >= NFO) ? S : S2) + (size_t)el * SEL + m;
                         cf[u] = coefS + ((f < 6) ? f : (f < NFO) ? f - 6 : 14 + (f - NFO));
                         acc[u] = 0.0;
@@ -769,9 +812,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                     for (int u = 0; u < PC; ++u) {
                         const int o = o0 + u * NL;
-                        if (o >= CT * nfo * NQ) continue;
+                        if (o >= CT * NF * NQ) continue;
                         const int m = o % NQ, rest = o / NQ;
-                        const int f = rest % nfo, el = rest / nfo;
+                        const int f = rest % NF, el = rest / NF;
                         const int col = el / T, r = el - col * T;
                         if (col < cols && r < rows) {
                             const int ip = i0 + col, jp = j0 + r;
@@ -787,6 +830,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         }
                     }
                 }
+                }
+                };
+                if (prm.half) node_fields(std::integral_constant<int, NFO + 2>{});
+                else node_fields(std::integral_constant<int, NFO>{});
                 // boundary closures: (element, face) items on physical boundary faces
                 for (int o = tid; o < CT * 4; o += NL) {
                     const int el = o >> 2, face = o & 3;

@@ -107,6 +107,8 @@ struct sweep_handle {
     int log2gb, gb, kpl, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
     size_t smem;
     int n_sm = 0;                 // SMs of the handle's device (queried at setup)
+    bool scan1d = false;          // 1-D: warp-scan kernel (k_1d.cu); the fixup keeps the sequential kernel
+    bool fused1d = false;         // 1-D scan: the last CTA sums the slabs (no finalize launch)
     sweepk::ReduceCaps caps{};    // grid caps of the reduction kernels
     // device workspace
     DirConst* d_dirs = nullptr;
@@ -586,6 +588,36 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             if ((ce = cudaMemset(h->d_ytag, 0xff, sizeof(int) * ntag)))
                 return cuda_fail(h, ce, "memset ytag"), bail(SWEEP_E_CUDA);
         }
+    } else if (!(h->opt & sweepk::OPT_FIXUP)) {
+        // warp-scan kernel: one warp per chain (direction, group), one lane per segment;
+        // a CTA = up to 8 chains of one half-range (its own slab)
+        h->scan1d = true;
+        int maxc = 1;
+        for (int q = 0; q < 2; ++q) maxc = std::max(maxc, (int)byq[q].size() * h->G);
+        const int W = std::min(8, maxc);
+        streams.clear();
+        for (int q = 0; q < 2; ++q) {
+            const int chains = (int)byq[q].size() * h->G;
+            for (int c0 = 0; c0 < chains; c0 += W) {
+                StreamDesc sdc;
+                sdc.quadrant = q;
+                sdc.d0 = qstart[q];
+                sdc.nd = (int)byq[q].size();
+                sdc.g0 = c0;
+                sdc.ng = std::min(W, chains - c0);
+                streams.push_back(sdc);
+            }
+        }
+        h->n_streams = (int)streams.size();
+        h->seglen = (h->nx + 31) / 32;
+        h->nseg = 32;
+        h->block = 32 * W;
+        const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
+        h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W);
+        h->grid = h->n_streams;
+        h->n_tasks = h->n_streams;
+        h->progress_ints = 0;
+        h->fused1d = (size_t)h->n_streams * h->sum_size <= 16384;
     } else {
         // segmented affine scan of the chain; the fixup is not affine: one segment
         h->nseg = (h->opt & sweepk::OPT_FIXUP) ? 1 : std::min(32, std::max(1, (h->nx + 15) / 16));
@@ -654,8 +686,9 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
     if (!guard.ok) return fail(h, SWEEP_E_CUDA, "cannot select device");
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t ce;
-    // reset progress flags and the task counter (the error flag is sticky until closures_get)
-    if ((ce = cudaMemsetAsync(h->d_progress, 0, sizeof(int) * (h->progress_ints + 1), st)))
+    // reset progress flags and the task counter (the error flag is sticky until closures_get);
+    // the 1-D scan kernel has no flags and resets its own completion counter
+    if (!h->scan1d && (ce = cudaMemsetAsync(h->d_progress, 0, sizeof(int) * (h->progress_ints + 1), st)))
         return cuda_fail(h, ce, "memset flags");
     if (h->d_ytag &&  // debug builds: tags of this run only
         (ce = cudaMemsetAsync(h->d_ytag, 0xff, sizeof(int) * (size_t)h->n_streams * 2 *
@@ -707,6 +740,27 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.nodes = h->nodes;
         prm.err = h->d_err;
         e = sweepk::launch_sweep2d(h->p, h->log2gb, h->kpl, h->opt, prm, h->grid, h->block, h->smem, stream);
+    } else if (h->scan1d) {
+        sweepk::Sweep1DScanParams prm;
+        prm.nx = h->nx;
+        prm.G = h->G;
+        prm.seglen = h->seglen;
+        prm.nodes = h->nodes;
+        prm.out_size = h->out_size;
+        prm.sum_size = h->sum_size;
+        prm.hr_off = h->off[7];
+        prm.inv_c_dt = inv_c_dt;
+        prm.sigma = d_sigma;
+        prm.q = d_q;
+        prm.inflow = d_inflow;
+        prm.dirs = h->d_dirs;
+        prm.streams = h->d_streams;
+        prm.slabs = h->d_slabs;
+        prm.err = h->d_err;
+        prm.done_counter = h->d_counter;
+        prm.fused_out = h->fused1d ? h->d_out : nullptr;
+        const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
+        e = sweepk::launch_sweep1d_scan(h->p, opt1, prm, h->grid, h->block, h->smem, stream);
     } else {
         sweepk::Sweep1DParams prm;
         prm.nx = h->nx;
@@ -733,7 +787,9 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
     ++h->launches;
     if (evs) cudaEventRecord(evs[1], st);
     const bool modal = (h->dim == 2 && h->p == 2);  // the p = 2 sweep leaves modal node fields in the slabs
-    if (!modal) {
+    if (h->fused1d) {
+        // summed by the sweep kernel's last CTA
+    } else if (!modal) {
         e = sweepk::launch_finalize(h->d_slabs, h->n_streams, h->out_size, h->sum_size, h->d_out, h->d_err,
                                     h->caps.finalize, stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "launch finalize");

@@ -90,6 +90,26 @@ struct Sweep1DParams {
     int* err;
 };
 
+// 1-D warp-scan sweep (k_1d.cu): one warp per chain (direction, group), one lane per segment
+struct Sweep1DScanParams {
+    int nx, G, seglen;             // seglen = ceil(nx / 32) elements per lane
+    size_t nodes, out_size, sum_size, hr_off;
+    double inv_c_dt;
+    const double* sigma;
+    const double* q;
+    const double* inflow;
+    const DirConst* dirs;
+    const StreamDesc* streams;     // per CTA: quadrant = half-range, d0 = its first direction,
+                                   // g0 / ng = first chain / chain count (chain j: d0 + j / G, group j % G)
+    double* slabs;                 // [grid][out_size]
+    int* err;
+    int* done_counter;             // fused_out: CTAs finished (the last one resets it)
+    double* fused_out;             // non-null: the last CTA sums the slabs' [0, sum_size) here
+};
+int scan1d_smem_bytes(int p, int opt, int warps);
+int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream);
+int upload_modal_1d(const ModalConsts& mc);
+
 // launchers (k_common.cu); return cudaError_t as int.  opt = OPT_* bits.
 int upload_modal(const ModalConsts& mc);
 int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, int grid, int block, size_t smem,
