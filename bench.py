@@ -329,7 +329,9 @@ def main():
     l2_bytes = 126 * 2 ** 20
     flush = torch.empty(0, dtype=torch.uint8, device=dev)
     if in_bytes < 2 * l2_bytes:
-        flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+        # 1 GiB (~0.17 ms of device time per step) also keeps the host's enqueue of the next
+        # step (Python + ctypes, tens of microseconds) off the device timeline of tiny configs
+        flush = torch.empty(1024 * 2 ** 20, dtype=torch.uint8, device=dev)
 
     if "trt" in opts:
         # NEXT-4: T^k per element of the config's recipe range, I^k = B_g(T^k) (input generation)
@@ -467,7 +469,7 @@ def main():
                        "unknowns": prob.unknowns, "groups_per_rank": g1 - g0,
                        "parallelism": f"group-sharded x{ws}" + (" + NCCL all-reduce" if ws > 1 else ""),
                        "l2": ("inputs %.2f GB > 126 MB L2, no flush" % (in_bytes / 1e9)) if not flush.numel()
-                       else "256 MB L2 flush before every step (outside the kernel timings)"},
+                       else "1 GiB L2 flush before every step (outside the step's events)"},
             "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_nominal, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_nominal,
                          "traffic": traffic["bytes_per_launch"] if traffic else None,

@@ -226,6 +226,10 @@ int scan1d_smem_bytes(int p, int opt, int warps) {
 
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream) {
     const void* f = (p == 2) ? pick_scan<2>(opt) : pick_scan<1>(opt);
+    if (smem > 48 * 1024) {
+        const int e = raise_smem_cap(f);
+        if (e) return e;
+    }
     void* args[] = {(void*)&prm};
     return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
 }

@@ -236,7 +236,7 @@ int sweep2d_cols_per_chunk(int p, int k, int opt) { return cols_per_chunk(p, k, 
 // The dynamic shared-memory cap is one value per kernel for the whole process, so it is
 // always raised to the device's opt-in maximum (never to one handle's size: a smaller
 // value set by a later handle would make an earlier handle's larger launch fail).
-static int raise_smem_cap(const void* f) {
+int raise_smem_cap(const void* f) {
     int dev = 0, optin = 0;
     cudaFuncAttributes fa;
     cudaError_t e = cudaGetDevice(&dev);

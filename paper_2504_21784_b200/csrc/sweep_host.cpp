@@ -822,7 +822,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
             return fail(h, SWEEP_E_NCCL, std::string("ncclAllReduce: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
     }
     if (evs) {
-        cudaEventRecord(evs[3], st);
+        if (h->comm) cudaEventRecord(evs[3], st);  // without a collective: no all-reduce interval
         ++h->runs_recorded;
     }
     return SWEEP_OK;
@@ -851,9 +851,11 @@ extern "C" int sweep_kernel_times(sweep_handle* h, double* ms, int max_runs, int
     const long long first = h->runs_recorded - n;
     for (int r = 0; r < n; ++r) {
         cudaEvent_t* e = &h->ev[(size_t)((first + r) % sweep_handle::kRing) * 4];
-        cudaError_t ce = cudaEventSynchronize(e[3]);
+        const int last = h->comm ? 3 : 2;
+        cudaError_t ce = cudaEventSynchronize(e[last]);
         if (ce) return cuda_fail(h, ce, "cudaEventSynchronize");
-        for (int k = 0; k < 3; ++k) {
+        ms[3 * r + 2] = 0.0;
+        for (int k = 0; k < last; ++k) {
             float t = 0;
             ce = cudaEventElapsedTime(&t, e[k], e[k + 1]);
             if (ce) return cuda_fail(h, ce, "cudaEventElapsedTime");

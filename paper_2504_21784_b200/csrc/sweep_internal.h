@@ -107,6 +107,7 @@ struct Sweep1DScanParams {
     double* fused_out;             // non-null: the last CTA sums the slabs' [0, sum_size) here
 };
 int scan1d_smem_bytes(int p, int opt, int warps);
+int raise_smem_cap(const void* f);  // dynamic smem cap of f := opt-in max - static smem
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream);
 int upload_modal_1d(const ModalConsts& mc);
 
