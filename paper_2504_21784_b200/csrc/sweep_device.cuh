@@ -119,6 +119,18 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int 
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
 }
+// 16-byte global->shared asynchronous copy (L2 only); both addresses 16-byte aligned
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+// 16-byte L2 load / store of a pair of doubles (the strip-boundary trace ring)
+__device__ __forceinline__ void ld_pair_cg(const double* p, double& a, double& b) {
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_pair(double* p, double a, double b) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -540,6 +552,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
     constexpr int C = cols_per_chunk(P, K, OPT);
     constexpr int CT = C * T;
     constexpr int NFIELD = 16;  // 6 moments + (beta, J+) x 4 faces + untraced P_xx, P_yy weights
+    // strip-boundary trace ring: per column, each lane's K*NT trace reals as KT2 pairs, laid
+    // out [pair][lane][2] (16-byte vector stores / loads / cp.async, coalesced per warp)
+    constexpr int KT = K * NT, KT2 = (KT + 1) / 2, RC = 2 * KT2;
 
     const int NL = blockDim.x;
     const int tid = threadIdx.x;
@@ -654,12 +669,12 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         stage(0, 0);
         // phase-C weights of this stream's directions: [dd][14]
         double* coefS = S + (size_t)CT * SEL;
-        double* ypre = coefS + dset * NFIELD;  // [K*NT][NL] next-column trace prefetch
+        double* ypre = coefS + ((dset * NFIELD + 1) & ~1);  // [KT2][NL][2] next-column trace prefetch (16-B aligned)
         constexpr int NFO = SIG ? 9 : 6;       // node fields: 6 moments (+ sigma phi, sigma Jx, sigma Jy)
         // SWEEP_HALF_RANGE: + the untraced P_xx, P_yy = sum w Omega_x^2 psi, sum w Omega_y^2 psi of
         // this stream (quadrant), into the stream slab's half-range rows (read by halfrange_kernel;
         // forming them as T + phi/3 there cancels when Omega^2 << 1/3)
-        double* bckS = ypre + K * NT * NL;     // [9][9] modal -> nodal (p = 2, boundary closures)
+        double* bckS = ypre + RC * NL;         // [9][9] modal -> nodal (p = 2, boundary closures)
         double* S2 = bckS + 81;                // SIG: [CT][SEL] sigma-weighted group sums
 #ifndef SWEEP_DEFER_C
 #define SWEEP_DEFER_C 1
@@ -766,6 +781,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         double acc[NF];
 #pragma unroll
                         for (int f = 0; f < NF; ++f) acc[f] = 0.0;
+#pragma unroll 4
                         for (int dd = 0; dd < sd.nd; ++dd) {
                             const double sv = Sp[dd * NQ];
                             const double sv2 = SIG ? Sp2[dd * NQ] : 0.0;
@@ -1009,8 +1025,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             if constexpr (P == 2) L = make_lane_p2(cx, cy, kap);
             else L = make_lane_p1(cx, cy, kap);
             const int nxp = prm.nx_pad;
-            const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)(K * NT) * NL;
-            double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)(K * NT) * NL;
+            const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)RC * NL;
+            double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)RC * NL;
             const bool write_y = J + 1 < prm.n_strips;
 #ifndef SWEEP_COL_UNROLL
 #define SWEEP_COL_UNROLL 1
@@ -1188,27 +1204,31 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     // (issued after this chunk's acquire), later columns from the private
                     // shared-memory slots the previous column prefetched with cp.async
 #ifdef SWEEP_DEBUG
-                    SWEEP_DCHECK(ysrc + ((size_t)ip + 1) * K * NT * NL <= prm.ytr + prm.ring_len);
+                    SWEEP_DCHECK(ysrc + ((size_t)ip + 1) * RC * NL <= prm.ytr + prm.ring_len);
                     SWEEP_DCHECK(__ldcg(prm.ytag + ((size_t)s * 2 + ((J + 1) & 1)) * nxp + ip) == J - 1);
 #endif
+                    double yt[RC];
                     if (col == 0) {
 #pragma unroll
-                        for (int k = 0; k < K; ++k)
-#pragma unroll
-                            for (int t = 0; t < NT; ++t)
-                                ty[k][t] = ld_hint(ysrc + ((size_t)ip * K + k) * NT * NL + t * NL + tid, pol_last);
+                        for (int pi = 0; pi < KT2; ++pi)
+                            ld_pair_cg(ysrc + (((size_t)ip * KT2 + pi) * NL + tid) * 2, yt[2 * pi], yt[2 * pi + 1]);
                     } else {
                         cp_async_wait<0>();
 #pragma unroll
-                        for (int k = 0; k < K; ++k)
-#pragma unroll
-                            for (int t = 0; t < NT; ++t) ty[k][t] = ypre[(k * NT + t) * NL + tid];
+                        for (int pi = 0; pi < KT2; ++pi) {
+                            const double2 v = *reinterpret_cast<const double2*>(ypre + ((size_t)pi * NL + tid) * 2);
+                            yt[2 * pi] = v.x;
+                            yt[2 * pi + 1] = v.y;
+                        }
                     }
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) ty[k][t] = yt[k * NT + t];
                     if (col + 1 < C) {
 #pragma unroll
-                        for (int kt = 0; kt < K * NT; ++kt)
-                            cp_async8_hint(ypre + kt * NL + tid, ysrc + ((size_t)(ip + 1) * K * NT + kt) * NL + tid,
-                                           pol_last);
+                        for (int pi = 0; pi < KT2; ++pi)
+                            cp_async16(ypre + ((size_t)pi * NL + tid) * 2, ysrc + (((size_t)(ip + 1) * KT2 + pi) * NL + tid) * 2);
                         cp_async_commit();
                     }
                 }
@@ -1272,13 +1292,17 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #else
                 if (write_y) {
 #endif
+                    double yt[RC];
 #pragma unroll
                     for (int k = 0; k < K; ++k)
 #pragma unroll
-                        for (int t = 0; t < NT; ++t)
-                            st_hint(ydst + ((size_t)ip * K + k) * NT * NL + t * NL + tid, ty[k][t], pol_last);
+                        for (int t = 0; t < NT; ++t) yt[k * NT + t] = ty[k][t];
+                    if constexpr (RC > KT) yt[RC - 1] = 0.0;
+#pragma unroll
+                    for (int pi = 0; pi < KT2; ++pi)
+                        st_pair(ydst + (((size_t)ip * KT2 + pi) * NL + tid) * 2, yt[2 * pi], yt[2 * pi + 1]);
 #ifdef SWEEP_DEBUG
-                    SWEEP_DCHECK(ydst + ((size_t)ip + 1) * K * NT * NL <= prm.ytr + prm.ring_len);
+                    SWEEP_DCHECK(ydst + ((size_t)ip + 1) * RC * NL <= prm.ytr + prm.ring_len);
                     if (tid == 0) __stcg(prm.ytag + ((size_t)s * 2 + (J & 1)) * nxp + ip, J);
 #endif
                 }

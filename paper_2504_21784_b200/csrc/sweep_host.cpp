@@ -578,7 +578,8 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->grid = std::min(h->n_tasks, bps * h->n_sm);
         const int NT = h->np1;
         h->progress_ints = (size_t)h->n_streams * h->n_strips;
-        h->ring_len = (size_t)h->n_streams * 2 * (h->n_chunks * C) * h->kpl * NT * h->block;
+        const int RC = 2 * ((h->kpl * NT + 1) / 2);  // ring record per lane: K*NT reals as pairs
+        h->ring_len = (size_t)h->n_streams * 2 * (h->n_chunks * C) * RC * h->block;
         if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * h->ring_len)))
             return cuda_fail(h, ce, "cudaMalloc ytr"), bail(SWEEP_E_CUDA);
         if (sweepk::debug_build()) {
