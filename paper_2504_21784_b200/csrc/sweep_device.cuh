@@ -1232,6 +1232,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         cp_async_commit();
                     }
                 }
+                // p = 1 without options: the group sums of the column's T elements are kept and
+                // reduced across the lanes of a direction together after the column (one
+                // reduce-scatter of T*NQ values: fewer shuffles, and off the row-to-row chain)
+                constexpr bool BATCH = (P == 1) && !SIG && LG > 1;
+                double usc[BATCH ? T * NQ : 1];
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
                     const int el = col * T + r;
@@ -1271,7 +1276,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         }
                     }
                     double* Sd = Sc + (size_t)el * SEL + dl * NQ;
-                    if constexpr (SIG) {
+                    if constexpr (BATCH) {
+#pragma unroll
+                        for (int m = 0; m < NQ; ++m) usc[r * NQ + m] = us[m];
+                    } else if constexpr (SIG) {
                         double* Sd2 = S2 + (size_t)el * SEL + dl * NQ;
                         auto sink = [&](int idx, double val) {
                             if (idx < NQ) Sd[idx] = val;
@@ -1286,6 +1294,14 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         if (lane == 0) Sd[0] = us[0] + us[1] + us[2] + us[3] + us[NQ - 1];
 #endif
                     }
+                }
+                if constexpr (BATCH) {
+                    // element r of this column: values [r NQ, (r+1) NQ) of usc
+                    auto sink = [&](int idx, double val) {
+                        const int r = idx / NQ;
+                        Sc[(size_t)(col * T + r) * SEL + dl * NQ + (idx - r * NQ)] = val;
+                    };
+                    ReduceScatter<T * NQ, LG / 2>::run(usc, lane, 0, T * NQ, sink);
                 }
 #ifdef SWEEP_ABL_NOYTR
                 if (false) {
