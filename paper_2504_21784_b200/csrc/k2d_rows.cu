@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) sweep2d_rows_kernel(const Sweep2DRowsPara
     }
     // inputs of sweep column ip of this row: sigma~ and q in sweep node order
     struct In {
-        double st, q[NN];
+        double st, q[NN], yin[NP1];  // yin: the physical y-inflow (bottom lane of block 0 only)
     };
     auto load = [&](int ip, In& x) {
         const int i = fx ? nx - 1 - ip : ip;
@@ -81,6 +81,13 @@ __global__ void __launch_bounds__(256) sweep2d_rows_kernel(const Sweep2DRowsPara
             const int aq = kk % NP1, bq = kk / NP1;
             const int a = fx ? P - aq : aq, bb = fy ? P - bq : bq;
             x.q[kk] = __ldg(prm.q + (e * NN + a + NP1 * bb) * G + g);
+        }
+        if (lane == 0 && b == 0) {
+#pragma unroll
+            for (int aq = 0; aq < NP1; ++aq) {
+                const int a = fx ? P - aq : aq;
+                x.yin[aq] = __ldg(prm.inflow + (size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g);
+            }
         }
     };
     // the element needed at step t is requested at step t - D into slot t % D
@@ -109,12 +116,8 @@ __global__ void __launch_bounds__(256) sweep2d_rows_kernel(const Sweep2DRowsPara
             double ty[NP1];
             if (lane == 0) {
                 if (b == 0) {
-                    const int i = fx ? nx - 1 - ip : ip;
 #pragma unroll
-                    for (int aq = 0; aq < NP1; ++aq) {
-                        const int a = fx ? P - aq : aq;
-                        ty[aq] = act ? prm.inflow[(size_t)bnode2d(fy ? 3 : 2, i, a, nx, ny, NP1) * G + g] : 0.0;
-                    }
+                    for (int aq = 0; aq < NP1; ++aq) ty[aq] = act ? cur.yin[aq] : 0.0;
                 } else {
 #pragma unroll
                     for (int aq = 0; aq < NP1; ++aq) ty[aq] = hand[(((size_t)((t + 1) & 1) * W + c) * nrb + b) * NP1 + aq];
