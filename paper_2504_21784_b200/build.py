@@ -14,7 +14,7 @@ DEBUG_LIB = os.path.join(HERE, "libsweep_debug.so")
 # device code is split over translation units that compile in parallel
 # (k2d_*.cu instantiate the 2-D kernel templates of sweep_device.cuh)
 SOURCES = [os.path.join(CSRC, f) for f in ("k2d_p2.cu", "k2d_opt_p2.cu", "k2d_p1.cu", "k2d_opt_p1.cu",
-                                           "k_common.cu", "k_1d.cu", "k2d_rows.cu", "k_trt.cu", "sweep_host.cpp")]
+                                           "k_common.cu", "k_1d.cu", "k_trt.cu", "sweep_host.cpp")]
 HEADERS = [os.path.join(CSRC, "sweep_internal.h"), os.path.join(CSRC, "sweep_device.cuh"),
            os.path.join(ROOT, "include", "sweep.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

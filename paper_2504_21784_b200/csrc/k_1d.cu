@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     constexpr int NP1 = P + 1;
     constexpr int NM = SIG ? 5 : 3;                  // phi, J, Txx (+ sigma phi, sigma J)
     constexpr int NV = (NM + (HALF ? 1 : 0)) * NP1;  // (+ P_xx)
-    constexpr int D = 4;                             // prefetch distance (elements)
+    constexpr int D = 8;                             // prefetch distance (elements): ~HBM latency / step
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int W = blockDim.x >> 5;
     const StreamDesc sd = prm.streams[blockIdx.x];   // quadrant = half-range; g0, ng = chain range
@@ -69,12 +69,13 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
 #pragma unroll
         for (int aq = 0; aq < NP1; ++aq) x.q[aq] = __ldg(prm.q + ((size_t)i * NP1 + (fx ? P - aq : aq)) * G + g);
     };
-    // software pipeline over the segment: element ip's inputs were requested D steps earlier
-    auto sweep_segment = [&](auto&& body) {
-        In buf[D];
+    // software pipeline over the segment: element ip's inputs were requested D steps earlier.
+    // A segment of at most D elements (C1) is loaded once: phase 3 reuses phase 1's buffer.
+    In buf[D];
+    auto sweep_segment = [&](bool preload, auto&& body) {
 #pragma unroll
         for (int u = 0; u < D; ++u)
-            if (on && e0 + u < e1) load(e0 + u, buf[u]);
+            if (preload && on && e0 + u < e1) load(e0 + u, buf[u]);
         for (int base = e0; base < e0 + L; base += D) {
 #pragma unroll
             for (int u = 0; u < D; ++u) {
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
 
     // ---- phase 1: compose this segment's affine maps
     double Tm = 1.0, Sm = 0.0;
-    sweep_segment([&](int ip, const In& x) {
+    sweep_segment(true, [&](int ip, const In& x) {
         if (!(on && ip < e1)) return;
         if (bad_sigma(x.st)) atomicOr(prm.err, 1);
         double psi[NP1], ta, sa;
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     double* slab = prm.slabs + (size_t)blockIdx.x * prm.out_size;
     const size_t sig_off = 3 * nodes + 4;  // after phi, J, Txx, beta[2], J+[2]
     int t = 0;
-    sweep_segment([&](int ip, const In& x) {
+    sweep_segment(L > D, [&](int ip, const In& x) {
         double v[NV];
         const bool live = on && ip < e1;
         if (live) {

@@ -109,8 +109,6 @@ struct sweep_handle {
     int n_sm = 0;                 // SMs of the handle's device (queried at setup)
     bool scan1d = false;          // 1-D: warp-scan kernel (k_1d.cu); the fixup keeps the sequential kernel
     bool fused1d = false;         // 1-D scan: the last CTA sums the slabs (no finalize launch)
-    bool rows2d = false;          // 2-D p = 1, few chains: row-wavefront kernel (k2d_rows.cu)
-    int rows_W = 0, rows_nrb = 0;
     sweepk::ReduceCaps caps{};    // grid caps of the reduction kernels
     // device workspace
     DirConst* d_dirs = nullptr;
@@ -564,41 +562,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         cuda_fail(h, (cudaError_t)re, "occupancy of the reduction kernels");
         return bail(SWEEP_E_CUDA);
     }
-    // 2-D p = 1 with few (direction, group) chains per quadrant: the row-wavefront kernel
-    // (the strip pipeline is latency bound there: one chain per lane, a CTA hand-off per chunk)
-    int chains_q = 0;
-    for (int q = 0; q < nquad; ++q) chains_q = std::max(chains_q, (int)byq[q].size() * h->G);
-    const int nrb = (h->ny + 31) / 32;
-    if (D.dim == 2 && D.p == 1 && h->opt == 0 && !(D.flags & SWEEP_HALF_RANGE) && chains_q <= 16 && nrb <= 8) {
-        const int W = std::max(1, std::min(8 / nrb, chains_q / 4));  // <= 8 warps per CTA
-        std::vector<StreamDesc> rs;
-        for (int q = 0; q < nquad; ++q) {
-            const int chains = (int)byq[q].size() * h->G;
-            for (int c0 = 0; c0 < chains; c0 += W) {
-                StreamDesc sdc;
-                sdc.quadrant = q;
-                sdc.d0 = qstart[q];
-                sdc.nd = (int)byq[q].size();
-                sdc.g0 = c0;
-                sdc.ng = std::min(W, chains - c0);
-                rs.push_back(sdc);
-            }
-        }
-        if ((double)rs.size() * (double)h->out_size <= 16.0 * 1024 * 1024) {
-            h->rows2d = true;
-            h->rows_W = W;
-            h->rows_nrb = nrb;
-            streams = rs;
-            h->n_streams = (int)rs.size();
-        }
-    }
-    if (h->rows2d) {
-        h->block = 32 * h->rows_W * h->rows_nrb;
-        h->smem = (size_t)sweepk::rows_smem_bytes(h->rows_W, h->rows_nrb);
-        h->grid = h->n_streams;
-        h->n_tasks = h->n_streams;
-        h->progress_ints = 0;
-    } else if (D.dim == 2) {
+    if (D.dim == 2) {
         const int T = sweepk::sweep2d_rows_per_strip(h->p, h->kpl), C = sweepk::sweep2d_cols_per_chunk(h->p, h->kpl, h->opt);
         h->n_strips = (h->ny + T - 1) / T;
         h->n_chunks = (h->nx + C - 1) / C;
@@ -725,7 +689,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
     cudaError_t ce;
     // reset progress flags and the task counter (the error flag is sticky until closures_get);
     // the 1-D scan kernel has no flags and resets its own completion counter
-    if (!h->scan1d && !h->rows2d && (ce = cudaMemsetAsync(h->d_progress, 0, sizeof(int) * (h->progress_ints + 1), st)))
+    if (!h->scan1d && (ce = cudaMemsetAsync(h->d_progress, 0, sizeof(int) * (h->progress_ints + 1), st)))
         return cuda_fail(h, ce, "memset flags");
     if (h->d_ytag &&  // debug builds: tags of this run only
         (ce = cudaMemsetAsync(h->d_ytag, 0xff, sizeof(int) * (size_t)h->n_streams * 2 *
@@ -739,26 +703,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         evs = &h->ev[(size_t)(h->runs_recorded % sweep_handle::kRing) * 4];
         cudaEventRecord(evs[0], st);
     }
-    if (h->rows2d) {
-        sweepk::Sweep2DRowsParams prm;
-        prm.nx = h->nx;
-        prm.ny = h->ny;
-        prm.G = h->G;
-        prm.W = h->rows_W;
-        prm.nrb = h->rows_nrb;
-        prm.nbnode = h->nbnode;
-        prm.nodes = h->nodes;
-        prm.out_size = h->out_size;
-        prm.inv_c_dt = inv_c_dt;
-        prm.sigma = d_sigma;
-        prm.q = d_q;
-        prm.inflow = d_inflow;
-        prm.dirs = h->d_dirs;
-        prm.streams = h->d_streams;
-        prm.slabs = h->d_slabs;
-        prm.err = h->d_err;
-        e = sweepk::launch_sweep2d_rows(prm, h->grid, h->block, h->smem, stream);
-    } else if (h->dim == 2) {
+    if (h->dim == 2) {
         sweepk::Sweep2DParams prm;
         prm.nx = h->nx;
         prm.ny = h->ny;

@@ -111,24 +111,6 @@ int raise_smem_cap(const void* f);  // dynamic smem cap of f := opt-in max - sta
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream);
 int upload_modal_1d(const ModalConsts& mc);
 
-// 2-D p = 1 with few chains per quadrant (k2d_rows.cu): warp = 32 rows of one chain
-// (direction, group), lane = row, anti-diagonal wavefront; CTA = W chains x nrb row blocks
-struct Sweep2DRowsParams {
-    int nx, ny, G, W, nrb, nbnode;
-    size_t nodes, out_size;
-    double inv_c_dt;
-    const double* sigma;
-    const double* q;
-    const double* inflow;
-    const DirConst* dirs;
-    const StreamDesc* streams;     // per CTA: quadrant, d0 = quadrant's first direction,
-                                   // g0 / ng = first chain / chain count (chain j: d0 + j / G, group j % G)
-    double* slabs;                 // [grid][out_size]
-    int* err;
-};
-int rows_smem_bytes(int W, int nrb);
-int launch_sweep2d_rows(const Sweep2DRowsParams& prm, int grid, int block, size_t smem, void* stream);
-
 // launchers (k_common.cu); return cudaError_t as int.  opt = OPT_* bits.
 int upload_modal(const ModalConsts& mc);
 int launch_sweep2d(int p, int log2lg, int k, int opt, const Sweep2DParams& prm, int grid, int block, size_t smem,
