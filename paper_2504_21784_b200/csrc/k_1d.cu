@@ -76,10 +76,11 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
 #pragma unroll
         for (int u = 0; u < D; ++u)
             if (preload && on && e0 + u < e1) load(e0 + u, buf[u]);
-        for (int base = e0; base < e0 + L; base += D) {
+        for (int t0 = 0; t0 < L; t0 += D) {
 #pragma unroll
             for (int u = 0; u < D; ++u) {
-                const int ip = base + u;
+                if (t0 + u >= L) break;  // uniform over the CTA (every lane has L steps)
+                const int ip = e0 + t0 + u;
                 In cur = buf[u];
                 if (on && ip + D < e1) load(ip + D, buf[u]);
                 cur.st = cur.sg + prm.inv_c_dt;

@@ -78,3 +78,59 @@ def test_shard_groups_balance():
             sizes = [b - a for a, b in parts]
             assert sum(sizes) == G and max(sizes) - min(sizes) <= 1
             assert parts[0][0] == 0 and all(parts[i][1] == parts[i + 1][0] for i in range(ws - 1))
+
+
+# ------------------------------------------------------------------ the product, 2 ranks on one GPU
+def _gpu_worker(rank: int, world: int, port: int, cfg: tuple, q):
+    """One rank of a group-sharded run through the product (libsweep via the binding): the
+    rank sweeps its group shard on cuda:0 (nranks = 1 inside the library: NCCL cannot put two
+    ranks on one device) and the ranks sum the gray outputs with gloo, as the NCCL all-reduce
+    of a multi-GPU run does on the device."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        import paper_2504_21784_b200 as pk
+        from bench import shard_groups
+        prob = synth.config(*cfg)
+        g0, g1 = shard_groups(prob.G, world, rank)
+        shard = prob.group_slice(g0, g1)
+        out = pk.run_problem(shard, device=0)
+        part = torch.from_numpy(out)
+        dist.all_reduce(part, op=dist.ReduceOp.SUM)
+        q.put((rank, part.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,cfg", [(2, (5, 16, 8)), (2, (4, 20, 6)), (2, (2, 128, 9))])
+def test_product_sharded_two_ranks_one_gpu(world, cfg):
+    import torch
+    import oracle
+    import synth
+    from tests.parity import assert_parity
+    import paper_2504_21784_b200 as pk
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device on a -m gpu run")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    prob = synth.config(*cfg)
+    full = pk.run_problem(prob, device=0)
+    ref = oracle.sweep(prob)
+    for _, got in res:
+        # sharded sum = one-rank result (to rounding of the different group partition) = oracle
+        assert np.abs(got - full).max() <= 1e-13 * np.abs(full).max()
+        assert_parity(got, ref, prob.dim, prob.nx, prob.ny, prob.p)
