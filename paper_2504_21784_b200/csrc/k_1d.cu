@@ -31,17 +31,24 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     constexpr int D = 8;                             // prefetch distance (elements): ~HBM latency / step
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int W = blockDim.x >> 5;
-    const StreamDesc sd = prm.streams[blockIdx.x];   // quadrant = half-range; g0, ng = chain range
-    const bool fx = (sd.quadrant & 1) != 0;
     const int nx = prm.nx, G = prm.G, L = prm.seglen;
     const size_t nodes = prm.nodes;
-    extern __shared__ __align__(16) double red[];    // [2][W][32][NV] + [W][4]
+    extern __shared__ __align__(16) double red[];    // [2][W][32][NV] + [W][4] (+ single: [NM][nodes])
     double* bred = red + 2 * (size_t)W * 32 * NV;
+    double* acc1 = bred + 4 * (size_t)W;             // single: the gray fields of the whole mesh
 
-    // this warp's chain
-    const int j = sd.g0 + w;
-    const bool on = w < sd.ng;
+    // this warp's chain.  Slab mode: the CTA's chains are one half-range's [g0, g0 + ng).
+    // Single mode (one CTA, tiny problems): warps [0, nw0) are the mu >= 0 chains, the rest the
+    // mu < 0 chains, and the gray fields are accumulated in shared memory (no slab, no finalize).
+    const bool single = prm.single != 0;
+    const StreamDesc sd = prm.streams[single ? (w >= prm.nw0 ? 1 : 0) : blockIdx.x];
+    const bool fx = (sd.quadrant & 1) != 0;
+    const int wl = single ? (w >= prm.nw0 ? w - prm.nw0 : w) : w;
+    const int j = sd.g0 + wl;
+    const bool on = wl < sd.ng;
     const int d = sd.d0 + (on ? j / G : 0), g = on ? j % G : 0;
+    if (single)
+        for (size_t k = tid; k < (size_t)NM * nodes; k += blockDim.x) acc1[k] = 0.0;
     double c = 0.0, cm[NM + 1], bw0 = 0.0, bw1 = 0.0, jw0 = 0.0, jw1 = 0.0;
 #pragma unroll
     for (int m = 0; m <= NM; ++m) cm[m] = 0.0;
@@ -158,6 +165,28 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
         __syncthreads();
         // sum over the CTA's chains (warp order) for the 32 elements of this step
         const double* rs = red + (size_t)(t & 1) * W * 32 * NV;
+        if (single) {
+            // per half-range (its own physical element at this step), added to the mesh fields;
+            // one thread per (segment, value) handles both halves: no two threads share an entry
+            for (int o = tid; o < 32 * NV; o += blockDim.x) {
+                const int s = o / NV, r = o - s * NV;
+                const int ips = s * L + t;
+                if (ips >= min(nx, (s + 1) * L)) continue;
+                const int m = r / NP1, aq = r - m * NP1;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int w0 = h ? prm.nw0 : 0, w1 = h ? W : prm.nw0;
+                    if (w0 >= w1) continue;
+                    double acc = 0.0;
+                    for (int ww = w0; ww < w1; ++ww) acc += rs[((size_t)ww * 32 + s) * NV + r];
+                    const int i = h ? nx - 1 - ips : ips;
+                    const int a = h ? P - aq : aq;
+                    acc1[(size_t)m * nodes + (size_t)i * NP1 + a] += acc;
+                }
+            }
+            ++t;
+            return;
+        }
         for (int o = tid; o < 32 * NV; o += blockDim.x) {
             const int s = o / NV, r = o - s * NV;
             const int ips = s * L + t;
@@ -185,7 +214,19 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
         double acc = 0.0;
         for (int ww = 0; ww < W; ++ww) acc += bred[ww * 4 + tid];
         // beta[x=0], beta[x=lx], J+[x=0], J+[x=lx]
-        slab[3 * nodes + tid] = acc;
+        (single ? prm.fused_out : slab)[3 * nodes + tid] = acc;
+    }
+    if (single) {
+        // the mesh fields straight to the packed output (rows phi, J, Txx [, sigma phi, sigma J])
+        bool bad = false;
+        for (size_t k = tid; k < (size_t)NM * nodes; k += blockDim.x) {
+            const size_t m = k / nodes, rest = k - m * nodes;
+            const double v = acc1[k];
+            prm.fused_out[(m < 3 ? m * nodes : sig_off + (m - 3) * nodes) + rest] = v;
+            bad |= !(fabs(v) < 1.0e300);
+        }
+        if (bad) atomicOr(prm.err, 2);
+        return;
     }
 
     // ---- fused final sum: the last CTA to finish sums the slabs in order (small outputs)
@@ -220,10 +261,10 @@ static const void* pick_scan(int opt) {
     }
 }
 
-int scan1d_smem_bytes(int p, int opt, int warps) {
+int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes) {
     const int nm = (opt & OPT_SIGMA) ? 5 : 3;
     const int nv = (nm + ((opt & OPT_HALF) ? 1 : 0)) * (p + 1);
-    return (int)sizeof(double) * (2 * warps * 32 * nv + warps * 4);
+    return (int)sizeof(double) * (2 * warps * 32 * nv + warps * 4 + nm * (int)single_nodes);
 }
 
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream) {

@@ -109,6 +109,8 @@ struct sweep_handle {
     int n_sm = 0;                 // SMs of the handle's device (queried at setup)
     bool scan1d = false;          // 1-D: warp-scan kernel (k_1d.cu); the fixup keeps the sequential kernel
     bool fused1d = false;         // 1-D scan: the last CTA sums the slabs (no finalize launch)
+    bool single1d = false;        // 1-D scan, tiny problem: one CTA for both half-ranges
+    int single_nw0 = 0;
     sweepk::ReduceCaps caps{};    // grid caps of the reduction kernels
     // device workspace
     DirConst* d_dirs = nullptr;
@@ -614,11 +616,34 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->nseg = 32;
         h->block = 32 * W;
         const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
-        h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W);
+        h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0);
         h->grid = h->n_streams;
         h->n_tasks = h->n_streams;
         h->progress_ints = 0;
         h->fused1d = (size_t)h->n_streams * h->sum_size <= 16384;
+        // tiny problems: every chain of both half-ranges in ONE CTA (<= 8 warps), the gray
+        // fields accumulated in shared memory: one launch, no slab, no cross-CTA sum
+        const int c0 = (int)byq[0].size() * h->G, c1 = (int)byq[1].size() * h->G;
+        if (!(h->flags & SWEEP_HALF_RANGE) && c0 + c1 <= 8 && h->nodes * 5 <= 8192) {
+            h->single1d = true;
+            h->single_nw0 = c0;
+            streams.clear();
+            for (int q = 0; q < 2; ++q) {
+                StreamDesc sdc;
+                sdc.quadrant = q;
+                sdc.d0 = qstart[q];
+                sdc.nd = (int)byq[q].size();
+                sdc.g0 = 0;
+                sdc.ng = (int)byq[q].size() * h->G;
+                streams.push_back(sdc);
+            }
+            h->n_streams = 2;
+            h->block = 32 * (c0 + c1);
+            h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, c0 + c1, h->nodes);
+            h->grid = 1;
+            h->n_tasks = 1;
+            h->fused1d = true;
+        }
     } else {
         // segmented affine scan of the chain; the fixup is not affine: one segment
         h->nseg = (h->opt & sweepk::OPT_FIXUP) ? 1 : std::min(32, std::max(1, (h->nx + 15) / 16));
@@ -760,6 +785,8 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.err = h->d_err;
         prm.done_counter = h->d_counter;
         prm.fused_out = h->fused1d ? h->d_out : nullptr;
+        prm.single = h->single1d ? 1 : 0;
+        prm.nw0 = h->single_nw0;
         const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
         e = sweepk::launch_sweep1d_scan(h->p, opt1, prm, h->grid, h->block, h->smem, stream);
     } else {

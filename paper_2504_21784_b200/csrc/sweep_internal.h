@@ -105,8 +105,10 @@ struct Sweep1DScanParams {
     int* err;
     int* done_counter;             // fused_out: CTAs finished (the last one resets it)
     double* fused_out;             // non-null: the last CTA sums the slabs' [0, sum_size) here
+    int single;                    // one CTA, both half-ranges (streams[0], streams[1]); fields
+    int nw0;                       // accumulated in shared memory, written to fused_out
 };
-int scan1d_smem_bytes(int p, int opt, int warps);
+int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes);
 int raise_smem_cap(const void* f);  // dynamic smem cap of f := opt-in max - static smem
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream);
 int upload_modal_1d(const ModalConsts& mc);
