@@ -111,6 +111,7 @@ struct sweep_handle {
     bool fused1d = false;         // 1-D scan: the last CTA sums the slabs (no finalize launch)
     bool single1d = false;        // 1-D scan, tiny problem: one CTA for both half-ranges
     int single_nw0 = 0;
+    bool stage1d = false;         // 1-D scan: inputs staged in shared memory
     sweepk::ReduceCaps caps{};    // grid caps of the reduction kernels
     // device workspace
     DirConst* d_dirs = nullptr;
@@ -616,7 +617,10 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->nseg = 32;
         h->block = 32 * W;
         const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
-        h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0);
+        const size_t stage = sweepk::scan1d_stage_doubles(h->p, h->nx, h->G, W);
+        const size_t smem_staged = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0, stage);
+        h->stage1d = stage > 0 && smem_staged <= 226 * 1024;  // opt-in maximum 227 KB
+        h->smem = h->stage1d ? smem_staged : (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0, 0);
         h->grid = h->n_streams;
         h->n_tasks = h->n_streams;
         h->progress_ints = 0;
@@ -639,7 +643,8 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             }
             h->n_streams = 2;
             h->block = 32 * (c0 + c1);
-            h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, c0 + c1, h->nodes);
+            h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, c0 + c1, h->nodes, 0);
+            h->stage1d = false;
             h->grid = 1;
             h->n_tasks = 1;
             h->fused1d = true;
@@ -787,6 +792,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.fused_out = h->fused1d ? h->d_out : nullptr;
         prm.single = h->single1d ? 1 : 0;
         prm.nw0 = h->single_nw0;
+        prm.stage = h->stage1d ? 1 : 0;
         const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
         e = sweepk::launch_sweep1d_scan(h->p, opt1, prm, h->grid, h->block, h->smem, stream);
     } else {

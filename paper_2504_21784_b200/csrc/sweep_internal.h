@@ -107,8 +107,10 @@ struct Sweep1DScanParams {
     double* fused_out;             // non-null: the last CTA sums the slabs' [0, sum_size) here
     int single;                    // one CTA, both half-ranges (streams[0], streams[1]); fields
     int nw0;                       // accumulated in shared memory, written to fused_out
+    int stage;                     // the CTA's inputs staged in shared memory (scan1d_stage_doubles)
 };
-int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes);
+int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes, size_t stage_doubles);
+size_t scan1d_stage_doubles(int p, int nx, int G, int warps);
 int raise_smem_cap(const void* f);  // dynamic smem cap of f := opt-in max - static smem
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream);
 int upload_modal_1d(const ModalConsts& mc);
