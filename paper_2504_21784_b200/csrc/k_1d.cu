@@ -79,17 +79,19 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     const int NG = min(G, W), g_lo = (G <= W) ? 0 : (sd.g0 % G);
     const int ELS = (NP1 + 1) * NG, SEGS = L * ELS + 1;
     if (staged) {
+        // asynchronous 8-byte copies: every thread's copies in flight at once (one latency)
         const int items = nx * (NP1 + 1) * NG;
-#pragma unroll 4
         for (int it = tid; it < items; it += blockDim.x) {
             const int gs = it % NG, rest = it / NG;
             const int v = rest % (NP1 + 1), ip = rest / (NP1 + 1);
             const int i = fx ? nx - 1 - ip : ip;
             const int gg = g_lo + gs;
-            const double val = (v == 0) ? __ldg(prm.sigma + (size_t)i * G + gg)
-                                        : __ldg(prm.q + ((size_t)i * NP1 + (fx ? P - (v - 1) : v - 1)) * G + gg);
-            stg[(size_t)(ip / L) * SEGS + (ip % L) * ELS + v * NG + gs] = val;
+            const double* src = (v == 0) ? prm.sigma + (size_t)i * G + gg
+                                         : prm.q + ((size_t)i * NP1 + (fx ? P - (v - 1) : v - 1)) * G + gg;
+            cp_async8(stg + (size_t)(ip / L) * SEGS + (ip % L) * ELS + v * NG + gs, src, 8);
         }
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncthreads();
     }
     // inputs of sweep-order element ip: sigma~, sigma, nodal q in sweep node order

@@ -518,6 +518,22 @@ __device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc,
 }
 #endif
 
+// Compile-time loop over the anti-diagonals DG, DG+1, ..., DGN-1 of a chunk: the body gets
+// the diagonal as an integral_constant, so its element count is a constant (batch sizes).
+template <int DG, int DGN>
+struct DiagLoop {
+    template <class F>
+    static __device__ __forceinline__ void run(F& f) {
+        f(std::integral_constant<int, DG>{});
+        DiagLoop<DG + 1, DGN>::run(f);
+    }
+};
+template <int DGN>
+struct DiagLoop<DGN, DGN> {
+    template <class F>
+    static __device__ __forceinline__ void run(F&) {}
+};
+
 // Lane layout: LG = 2^LOG2LG consecutive lanes share one direction and hold
 // consecutive groups; each lane carries K groups (g, g + LG, ...), so a stream
 // (CTA) covers GBK = LG*K groups of NL/LG directions.  The K independent solves
@@ -1035,15 +1051,15 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #ifndef SWEEP_SKEW_K1
 #define SWEEP_SKEW_K1 1
 #endif
-            if constexpr (K == 1 && LG == 1 && SWEEP_SKEW_K1 && !FIX) {
-                // one group per direction (C3): a lane has a single solve chain per element,
-                // so the chunk is swept along its anti-diagonals (element (r, col) needs only
-                // (r - 1, col) and (r, col - 1)); the up to min(T, C) solves of a diagonal
-                // are independent and the fully unrolled code interleaves them.  The
-                // y-traces of all C columns are loaded up front (one L2 round trip per chunk).
-                // Measured: C3 0.349 -> 0.321 ms; with a group reduction per element (LG > 1:
-                // C4, the 8- and 16-group ranks of C5) it was 3-16 % slower, so those keep
-                // the column loop.
+            if constexpr (K == 1 && (LG == 1 || (P == 1 && !SIG)) && SWEEP_SKEW_K1 && !FIX) {
+                // one group per lane: a lane has a single solve chain per element, so the chunk
+                // is swept along its anti-diagonals (element (r, col) needs only (r - 1, col)
+                // and (r, col - 1)); the up to min(T, C) solves of a diagonal are independent
+                // and the fully unrolled code interleaves them.  The y-traces of all C columns
+                // are loaded up front (one L2 round trip per chunk).  C3 (LG = 1): 0.349 ->
+                // 0.321 ms (round 1).  With a group reduction (LG > 1, p = 1: C4) the group sums
+                // of a diagonal's elements are reduced across the lanes of a direction in one
+                // reduce-scatter after the diagonal (per element it was 3-16 % slower).
                 double tyc[C][NT];
                 if (J == 0) {
 #pragma unroll
@@ -1080,12 +1096,15 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         for (int t = 0; t < NT; ++t)
                             tyc[col][t] = ld_hint(ysrc + (size_t)(i0 + col) * NT * NL + t * NL + tid, pol_last);
                 }
+                auto diag = [&](auto dgc) {
+                    constexpr int dg = decltype(dgc)::value;
+                    constexpr int rlo = (dg - (C - 1) > 0) ? dg - (C - 1) : 0;
+                    constexpr int rhi = (dg < T - 1) ? dg : T - 1;
+                    constexpr int NB = rhi - rlo + 1;  // elements on this diagonal
+                    double ub[NB * NQ];
 #pragma unroll
-                for (int dg = 0; dg < T + C - 1; ++dg) {
-#pragma unroll
-                    for (int r = 0; r < T; ++r) {
+                    for (int r = rlo; r <= rhi; ++r) {
                         const int col = dg - r;
-                        if (col < 0 || col >= C) continue;
                         const int el = col * T + r;
                         double qh[NQ], u[NQ], txo[NT], tyo[NT];
 #pragma unroll
@@ -1099,7 +1118,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             tyc[col][t] = tyo[t];
                         }
                         double* Sd = Sc + (size_t)el * SEL + dl * NQ;
-                        if constexpr (SIG) {
+                        if constexpr (LG > 1) {
+#pragma unroll
+                            for (int m = 0; m < NQ; ++m) ub[(r - rlo) * NQ + m] = u[m];
+                        } else if constexpr (SIG) {
                             double us[2 * NQ];
 #pragma unroll
                             for (int m = 0; m < NQ; ++m) {
@@ -1117,7 +1139,16 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             ReduceScatter<NQ, LG / 2>::run(u, lane, 0, NQ, sink);
                         }
                     }
-                }
+                    if constexpr (LG > 1) {
+                        // element rlo + b of this diagonal: values [b NQ, (b+1) NQ) of ub
+                        auto sink = [&](int idx, double val) {
+                            const int r = rlo + idx / NQ;
+                            Sc[(size_t)((dg - r) * T + r) * SEL + dl * NQ + (idx % NQ)] = val;
+                        };
+                        ReduceScatter<NB * NQ, LG / 2>::run(ub, lane, 0, NB * NQ, sink);
+                    }
+                };
+                DiagLoop<0, T + C - 1>::run(diag);
                 if (write_y) {
 #pragma unroll
                     for (int col = 0; col < C; ++col)
