@@ -188,6 +188,16 @@ int trt_step(sweep_handle *h, const double *d_sigma, const double *d_inflow, con
  * out[6] lanes per direction, out[7] SMs of the device. */
 int sweep_stats(const sweep_handle *h, long long out[8]);
 
+/* Device cross-check of the element solves (a plain register LU kept as a
+ * reference variant inside the GPU build): n random element systems in sweep coordinates
+ * (sigma~ I + cx A (x) I + cy I (x) A) psi = q + lifts (the lumped weak form of
+ * eq:dgsn_transport, in the scaled form of DESIGN.md §4), sigma~ in
+ * [0.1, 1e4], cx, cy = |Omega|/h with h = 1/512, each solved on the device both by dense
+ * Gaussian elimination of the assembled (p+1)^2 system and by the structured solve of the
+ * sweep (p = 1 closed form, p = 2 modal).  *max_rel_err = the largest max-norm relative
+ * difference of the nodal solutions.  seed selects the systems (counter-based generator). */
+int sweep_selfcheck_solves(int device, int p, int n, unsigned long long seed, double *max_rel_err);
+
 /* Launch-latency floor of the device: back-to-back launches of an empty kernel on one
  * stream, device time per launch in microseconds (the floor the latency-bound configs
  * C1-C3 are reported against). */

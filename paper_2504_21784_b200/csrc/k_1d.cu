@@ -17,8 +17,6 @@
 // in a fixed order by the last CTA to finish when they are small (one launch per sweep),
 // else by the finalize kernel.  The zero-and-scale fixup is not affine: it keeps the
 // sequential kernel (sweep1d_kernel).
-#include <algorithm>
-
 #include "sweep_device.cuh"
 
 namespace sweepk {
@@ -38,7 +36,6 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     extern __shared__ __align__(16) double red[];    // [2][W][32][NV] + [W][4] (+ single: [NM][nodes])
     double* bred = red + 2 * (size_t)W * 32 * NV;
     double* acc1 = bred + 4 * (size_t)W;             // single: the gray fields of the whole mesh
-    double* stg = acc1;                              // staged: the CTA's sigma and q (not with single)
 
     // this warp's chain.  Slab mode: the CTA's chains are one half-range's [g0, g0 + ng).
     // Single mode (one CTA, tiny problems): warps [0, nw0) are the mu >= 0 chains, the rest the
@@ -69,43 +66,11 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     }
     const int e0 = min(nx, lane * L), e1 = min(nx, e0 + L);  // this lane's segment (sweep order)
 
-    // Staged mode (prm.stage, the CTA's chains share NG <= W consecutive groups): the CTA's
-    // sigma and q of the whole mesh are copied once, coalesced (the group rows of an element are
-    // contiguous), into shared memory, [segment][element of segment][sigma, q_0, .., q_P][group];
-    // the segment stride is odd so the 32 lanes (segments) of a warp hit distinct banks.
-    // Without it each lane's 8-byte loads touch a 32-byte sector of their own (C2: 4x the L2
-    // traffic, and every element is read again by each of the 16 directions).
-    const bool staged = prm.stage != 0 && !single;
-    const int NG = min(G, W), g_lo = (G <= W) ? 0 : (sd.g0 % G);
-    const int ELS = (NP1 + 1) * NG, SEGS = L * ELS + 1;
-    if (staged) {
-        // asynchronous 8-byte copies: every thread's copies in flight at once (one latency)
-        const int items = nx * (NP1 + 1) * NG;
-        for (int it = tid; it < items; it += blockDim.x) {
-            const int gs = it % NG, rest = it / NG;
-            const int v = rest % (NP1 + 1), ip = rest / (NP1 + 1);
-            const int i = fx ? nx - 1 - ip : ip;
-            const int gg = g_lo + gs;
-            const double* src = (v == 0) ? prm.sigma + (size_t)i * G + gg
-                                         : prm.q + ((size_t)i * NP1 + (fx ? P - (v - 1) : v - 1)) * G + gg;
-            cp_async8(stg + (size_t)(ip / L) * SEGS + (ip % L) * ELS + v * NG + gs, src, 8);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-    }
     // inputs of sweep-order element ip: sigma~, sigma, nodal q in sweep node order
     struct In {
         double st, sg, q[NP1];
     };
     auto load = [&](int ip, In& x) {
-        if (staged) {
-            const double* sp = stg + (size_t)(ip / L) * SEGS + (ip % L) * ELS + (g - g_lo);
-            x.sg = sp[0];
-#pragma unroll
-            for (int aq = 0; aq < NP1; ++aq) x.q[aq] = sp[(aq + 1) * NG];
-            return;
-        }
         const int i = fx ? nx - 1 - ip : ip;
         x.sg = __ldg(prm.sigma + (size_t)i * G + g);
 #pragma unroll
@@ -296,19 +261,10 @@ static const void* pick_scan(int opt) {
     }
 }
 
-int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes, size_t stage_doubles) {
+int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes) {
     const int nm = (opt & OPT_SIGMA) ? 5 : 3;
     const int nv = (nm + ((opt & OPT_HALF) ? 1 : 0)) * (p + 1);
-    const size_t tail = std::max((size_t)nm * single_nodes, stage_doubles);
-    return (int)(sizeof(double) * (2 * (size_t)warps * 32 * nv + warps * 4 + tail));
-}
-
-// doubles of the staged inputs of one CTA (k_1d.cu layout), 0 if not applicable
-size_t scan1d_stage_doubles(int p, int nx, int G, int warps) {
-    const int ng = G < warps ? G : warps;
-    if (G > warps && G % warps) return 0;  // a CTA's chains would straddle two directions
-    const int L = (nx + 31) / 32;
-    return (size_t)32 * ((size_t)L * (p + 2) * ng + 1);
+    return (int)(sizeof(double) * (2 * (size_t)warps * 32 * nv + warps * 4 + (size_t)nm * single_nodes));
 }
 
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream) {

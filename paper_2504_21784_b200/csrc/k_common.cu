@@ -1,5 +1,7 @@
 // k_common.cu — the 1-D sweep kernels, the slab reduction, the FP64 probe and the
 // launch dispatch over the 2-D translation units (k2d_*.cu).
+#include <cstring>
+
 #include "sweep_device.cuh"
 
 namespace sweepk {
@@ -359,6 +361,126 @@ int debug_build() { return 1; }
 #else
 int debug_build() { return 0; }
 #endif
+
+// ------------------------------------------------------------------ device cross-check of the solves
+// SURVEY §7 hard part 1: "keep a plain register LU without pivoting as a reference variant
+// inside the GPU code".  Each thread draws a random element system in sweep coordinates,
+//     (sigma~ I + cx A^ (x) I + cy I (x) A^) psi = q + lifts   (SV F1),
+// assembles it densely from the reference matrix A^ (nodes k = a + (p+1) b), solves it by
+// Gaussian elimination without pivoting (the symmetric part is positive definite, SV §8c),
+// and compares the nodal solution with the structured solve the sweep uses: solve_p1 (the
+// closed-form inverse, SV F4) or solve_p2 (modal: q and the inflow traces transformed with W,
+// the solution back with V, SV F5).  The largest relative difference (max-norm per system)
+// is returned through an atomicMax on its bit pattern.
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long& x) {
+    unsigned long long z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double urand(unsigned long long& x) { return (double)(splitmix(x) >> 11) * 0x1.0p-53; }
+
+template <int P>
+__global__ void selfcheck_solves_kernel(int n, unsigned long long seed, unsigned long long* worst) {
+    constexpr int NP1 = P + 1, N = NP1 * NP1;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    unsigned long long rs = seed * 0x2545F4914F6CDD1Dull + (unsigned long long)t;
+    // C4/C5 ranges: sigma~ log-uniform in [0.1, 1e4], |Omega_x|, |Omega_y| in [0.01, 1], h = 1/512
+    const double st = exp(log(0.1) + urand(rs) * (log(1e4) - log(0.1)));
+    const double cx = (0.01 + 0.99 * urand(rs)) * 512.0, cy = (0.01 + 0.99 * urand(rs)) * 512.0;
+    double q[N], tx[NP1], ty[NP1];
+    for (int k = 0; k < N; ++k) q[k] = urand(rs) * 10.0;
+    for (int k = 0; k < NP1; ++k) {
+        tx[k] = urand(rs) * 10.0;
+        ty[k] = urand(rs) * 10.0;
+    }
+    // dense system from A^ and the GLL inflow weight w0 = 1/2 (p = 1), 1/6 (p = 2)
+    double Ah[NP1][NP1];
+    if constexpr (P == 1) {
+        const double a1[2][2] = {{1, 1}, {-1, 1}};
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) Ah[i][j] = a1[i][j];
+    } else {
+        const double a2[3][3] = {{3, 4, -1}, {-1, 0, 1}, {1, -4, 3}};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) Ah[i][j] = a2[i][j];
+    }
+    const double lift = (P == 1) ? 2.0 : 6.0;
+    double M[N][N], rhs[N];
+    for (int k = 0; k < N; ++k) {
+        const int a = k % NP1, b = k / NP1;
+        for (int l = 0; l < N; ++l) {
+            const int a2 = l % NP1, b2 = l / NP1;
+            double v = (k == l) ? st : 0.0;
+            if (b == b2) v += cx * Ah[a][a2];
+            if (a == a2) v += cy * Ah[b][b2];
+            M[k][l] = v;
+        }
+        rhs[k] = q[k] + ((a == 0) ? lift * cx * tx[b] : 0.0) + ((b == 0) ? lift * cy * ty[a] : 0.0);
+    }
+    for (int c = 0; c < N; ++c) {  // Gaussian elimination, no pivoting
+        const double inv = 1.0 / M[c][c];
+        for (int r = c + 1; r < N; ++r) {
+            const double f = M[r][c] * inv;
+            for (int l = c; l < N; ++l) M[r][l] -= f * M[c][l];
+            rhs[r] -= f * rhs[c];
+        }
+    }
+    double x[N];
+    for (int r = N - 1; r >= 0; --r) {
+        double acc = rhs[r];
+        for (int l = r + 1; l < N; ++l) acc -= M[r][l] * x[l];
+        x[r] = acc / M[r][r];
+    }
+    // the structured solve
+    double psi[N];
+    if constexpr (P == 1) {
+        const LaneP1 L = make_lane_p1(cx, cy);
+        double u[4], txo[2], tyo[2];
+        solve_p1(L, st, q, tx, ty, u, txo, tyo);
+        for (int k = 0; k < 4; ++k) psi[k] = u[k];
+    } else {
+        const LaneP2 L = make_lane_p2(cx, cy);
+        double qh[9], txm[3], tym[3], u[9], txo[3], tyo[3];
+        modal_forward(q, qh);
+        txm[0] = cM.W0[0] * tx[0] + cM.W0[1] * tx[1] + cM.W0[2] * tx[2];
+        txm[1] = cM.W1re[0] * tx[0] + cM.W1re[1] * tx[1] + cM.W1re[2] * tx[2];
+        txm[2] = cM.W1im[0] * tx[0] + cM.W1im[1] * tx[1] + cM.W1im[2] * tx[2];
+        tym[0] = cM.W0[0] * ty[0] + cM.W0[1] * ty[1] + cM.W0[2] * ty[2];
+        tym[1] = cM.W1re[0] * ty[0] + cM.W1re[1] * ty[1] + cM.W1re[2] * ty[2];
+        tym[2] = cM.W1im[0] * ty[0] + cM.W1im[1] * ty[1] + cM.W1im[2] * ty[2];
+        solve_p2(L, st, qh, txm, tym, u, txo, tyo);
+        modal_to_nodal_p2(u, psi);
+    }
+    double dm = 0.0, xm = 0.0;
+    for (int k = 0; k < N; ++k) {
+        dm = fmax(dm, fabs(psi[k] - x[k]));
+        xm = fmax(xm, fabs(x[k]));
+    }
+    const double rel = (xm > 0.0) ? dm / xm : dm;
+    atomicMax(worst, (unsigned long long)__double_as_longlong(rel));  // rel >= 0: bits are monotone
+}
+
+int selfcheck_solves(int device, int p, int n, unsigned long long seed, double* max_rel) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e) return (int)e;
+    unsigned long long* d = nullptr;
+    if ((e = cudaMalloc(&d, sizeof(unsigned long long)))) return (int)e;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    const int block = 128, grid = (n + block - 1) / block;
+    if (p == 2) selfcheck_solves_kernel<2><<<grid, block>>>(n, seed, d);
+    else selfcheck_solves_kernel<1><<<grid, block>>>(n, seed, d);
+    unsigned long long h = 0;
+    e = cudaGetLastError();
+    if (!e) e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e) return (int)e;
+    double r;
+    memcpy(&r, &h, sizeof r);
+    *max_rel = r;
+    return 0;
+}
 
 // empty-kernel launch floor: reps back-to-back launches of an empty kernel on one stream,
 // timed with events on that stream (device-side time per launch, host enqueue overlapped)

@@ -1051,15 +1051,15 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #ifndef SWEEP_SKEW_K1
 #define SWEEP_SKEW_K1 1
 #endif
-            if constexpr (K == 1 && (LG == 1 || (P == 1 && !SIG)) && SWEEP_SKEW_K1 && !FIX) {
+            if constexpr (K == 1 && LG == 1 && SWEEP_SKEW_K1 && !FIX) {
                 // one group per lane: a lane has a single solve chain per element, so the chunk
                 // is swept along its anti-diagonals (element (r, col) needs only (r - 1, col)
                 // and (r, col - 1)); the up to min(T, C) solves of a diagonal are independent
                 // and the fully unrolled code interleaves them.  The y-traces of all C columns
                 // are loaded up front (one L2 round trip per chunk).  C3 (LG = 1): 0.349 ->
-                // 0.321 ms (round 1).  With a group reduction (LG > 1, p = 1: C4) the group sums
-                // of a diagonal's elements are reduced across the lanes of a direction in one
-                // reduce-scatter after the diagonal (per element it was 3-16 % slower).
+                // 0.321 ms (round 1).  With a group reduction (LG > 1) the column loop is faster:
+                // per-element reductions 3-16 % (round 1), per-diagonal batched reductions 2 %
+                // (C4 0.899 vs 0.880 ms, round 2).
                 double tyc[C][NT];
                 if (J == 0) {
 #pragma unroll
@@ -1100,8 +1100,6 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     constexpr int dg = decltype(dgc)::value;
                     constexpr int rlo = (dg - (C - 1) > 0) ? dg - (C - 1) : 0;
                     constexpr int rhi = (dg < T - 1) ? dg : T - 1;
-                    constexpr int NB = rhi - rlo + 1;  // elements on this diagonal
-                    double ub[NB * NQ];
 #pragma unroll
                     for (int r = rlo; r <= rhi; ++r) {
                         const int col = dg - r;
@@ -1118,10 +1116,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             tyc[col][t] = tyo[t];
                         }
                         double* Sd = Sc + (size_t)el * SEL + dl * NQ;
-                        if constexpr (LG > 1) {
-#pragma unroll
-                            for (int m = 0; m < NQ; ++m) ub[(r - rlo) * NQ + m] = u[m];
-                        } else if constexpr (SIG) {
+                        if constexpr (SIG) {
                             double us[2 * NQ];
 #pragma unroll
                             for (int m = 0; m < NQ; ++m) {
@@ -1138,14 +1133,6 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                             auto sink = [&](int idx, double val) { Sd[idx] = val; };
                             ReduceScatter<NQ, LG / 2>::run(u, lane, 0, NQ, sink);
                         }
-                    }
-                    if constexpr (LG > 1) {
-                        // element rlo + b of this diagonal: values [b NQ, (b+1) NQ) of ub
-                        auto sink = [&](int idx, double val) {
-                            const int r = rlo + idx / NQ;
-                            Sc[(size_t)((dg - r) * T + r) * SEL + dl * NQ + (idx % NQ)] = val;
-                        };
-                        ReduceScatter<NB * NQ, LG / 2>::run(ub, lane, 0, NB * NQ, sink);
                     }
                 };
                 DiagLoop<0, T + C - 1>::run(diag);

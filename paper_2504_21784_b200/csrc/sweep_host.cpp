@@ -111,7 +111,6 @@ struct sweep_handle {
     bool fused1d = false;         // 1-D scan: the last CTA sums the slabs (no finalize launch)
     bool single1d = false;        // 1-D scan, tiny problem: one CTA for both half-ranges
     int single_nw0 = 0;
-    bool stage1d = false;         // 1-D scan: inputs staged in shared memory
     sweepk::ReduceCaps caps{};    // grid caps of the reduction kernels
     // device workspace
     DirConst* d_dirs = nullptr;
@@ -617,10 +616,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
         h->nseg = 32;
         h->block = 32 * W;
         const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
-        const size_t stage = sweepk::scan1d_stage_doubles(h->p, h->nx, h->G, W);
-        const size_t smem_staged = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0, stage);
-        h->stage1d = stage > 0 && smem_staged <= 226 * 1024;  // opt-in maximum 227 KB
-        h->smem = h->stage1d ? smem_staged : (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0, 0);
+        h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, W, 0);
         h->grid = h->n_streams;
         h->n_tasks = h->n_streams;
         h->progress_ints = 0;
@@ -643,8 +639,7 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             }
             h->n_streams = 2;
             h->block = 32 * (c0 + c1);
-            h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, c0 + c1, h->nodes, 0);
-            h->stage1d = false;
+            h->smem = (size_t)sweepk::scan1d_smem_bytes(h->p, opt1, c0 + c1, h->nodes);
             h->grid = 1;
             h->n_tasks = 1;
             h->fused1d = true;
@@ -792,7 +787,6 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.fused_out = h->fused1d ? h->d_out : nullptr;
         prm.single = h->single1d ? 1 : 0;
         prm.nw0 = h->single_nw0;
-        prm.stage = h->stage1d ? 1 : 0;
         const int opt1 = h->opt | ((h->flags & SWEEP_HALF_RANGE) ? sweepk::OPT_HALF : 0);
         e = sweepk::launch_sweep1d_scan(h->p, opt1, prm, h->grid, h->block, h->smem, stream);
     } else {
@@ -1029,6 +1023,26 @@ extern "C" int sweep_stats(const sweep_handle* h, long long out[8]) {
     out[5] = (h->dim == 2) ? h->kpl : 1;
     out[6] = h->gb;
     out[7] = h->n_sm;
+    return SWEEP_OK;
+}
+
+extern "C" int sweep_selfcheck_solves(int device, int p, int n, unsigned long long seed, double* max_rel_err) {
+    if (!max_rel_err || (p != 1 && p != 2) || n < 1) return SWEEP_E_ARG;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    // the p = 2 check needs the modal constants of the library's own setup
+    ModalConsts mc;
+    memset(&mc, 0, sizeof mc);
+    std::string err;
+    int e = 0;
+    if (!build_modal(mc, err)) {
+        if (prev >= 0) cudaSetDevice(prev);
+        return fail(nullptr, SWEEP_E_INTERNAL, err);
+    }
+    if (!(e = cudaSetDevice(device))) e = sweepk::upload_modal(mc);
+    if (!e) e = sweepk::selfcheck_solves(device, p, n, seed, max_rel_err);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (e) return fail(nullptr, SWEEP_E_CUDA, std::string("selfcheck: ") + sweepk::cuda_err_string(e));
     return SWEEP_OK;
 }
 

@@ -107,10 +107,8 @@ struct Sweep1DScanParams {
     double* fused_out;             // non-null: the last CTA sums the slabs' [0, sum_size) here
     int single;                    // one CTA, both half-ranges (streams[0], streams[1]); fields
     int nw0;                       // accumulated in shared memory, written to fused_out
-    int stage;                     // the CTA's inputs staged in shared memory (scan1d_stage_doubles)
 };
-int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes, size_t stage_doubles);
-size_t scan1d_stage_doubles(int p, int nx, int G, int warps);
+int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes);
 int raise_smem_cap(const void* f);  // dynamic smem cap of f := opt-in max - static smem
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream);
 int upload_modal_1d(const ModalConsts& mc);
@@ -139,6 +137,7 @@ int sweep2d_cols_per_chunk(int p, int k, int opt);
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
 int launch_floor(int device, int reps, double* us);
+int selfcheck_solves(int device, int p, int n, unsigned long long seed, double* max_rel);
 int debug_build();  // 1 in -DSWEEP_DEBUG builds (bounds checks + trace-ring tags)
 
 // unaccelerated TRT iteration (k_trt.cu)

@@ -26,7 +26,8 @@ _NAMES = {1: "E_ARG", 2: "E_QUAD", 3: "E_SIGMA", 4: "E_CUDA", 5: "E_NCCL", 6: "E
 # every symbol include/sweep.h declares
 EXPORTS = ("sweep_setup", "sweep_layout", "sweep_run", "closures_get", "sweep_run_host", "trt_step",
            "sweep_stats", "sweep_timing", "sweep_kernel_times", "sweep_fp64_probe",
-           "sweep_nccl_unique_id", "sweep_destroy", "sweep_last_error", "sweep_launch_floor")
+           "sweep_nccl_unique_id", "sweep_destroy", "sweep_last_error", "sweep_launch_floor",
+           "sweep_selfcheck_solves")
 
 
 class SweepError(RuntimeError):
@@ -87,6 +88,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.sweep_kernel_times.restype = i
         lib.sweep_fp64_probe.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
         lib.sweep_fp64_probe.restype = i
+        lib.sweep_selfcheck_solves.argtypes = [i, i, i, ctypes.c_ulonglong, ctypes.POINTER(ctypes.c_double)]
+        lib.sweep_selfcheck_solves.restype = i
         lib.sweep_launch_floor.argtypes = [i, i, ctypes.POINTER(ctypes.c_double)]
         lib.sweep_launch_floor.restype = i
         lib.sweep_nccl_unique_id.argtypes = [vp]
@@ -127,6 +130,17 @@ def launch_floor(device: int = 0, reps: int = 2000) -> float:
     if rc:
         raise SweepError(rc, lib.sweep_last_error(None).decode())
     return t.value
+
+
+def selfcheck_solves(p: int, n: int = 1 << 20, seed: int = 1, device: int = 0) -> float:
+    """Largest relative difference between the sweep's structured element solves and a plain
+    dense LU of the same random element systems, both on the device (include/sweep.h)."""
+    lib = load_library()
+    r = ctypes.c_double()
+    rc = lib.sweep_selfcheck_solves(device, p, n, seed, ctypes.byref(r))
+    if rc:
+        raise SweepError(rc, lib.sweep_last_error(None).decode())
+    return r.value
 
 
 def _dptr(a: np.ndarray):
