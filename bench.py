@@ -272,6 +272,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--rank-of", type=int, default=1,
+                    help="analysis: on one GPU, sweep only the group shard rank 0 of a K-rank group split owns "
+                         "(the per-rank workload of the strong-scaling run, without the all-reduce)")
     ap.add_argument("--lib", default=None, help="another build of libsweep.so (experiment builds only, "
                                                   "scripts/build_variants.py)")
     ap.add_argument("--opts", default="", help="comma list of NEXT-row options: sigma (sigma-weighted moments), "
@@ -309,8 +312,11 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     prob = synth.config(args.config)
-    g0, g1 = shard_groups(prob.G, ws, rank)
+    if args.rank_of > 1 and ws > 1:
+        ap.error("--rank-of is a one-process analysis mode")
+    g0, g1 = shard_groups(prob.G, max(ws, args.rank_of), rank)
     shard = prob.group_slice(g0, g1)
+    job_unknowns = prob.unknowns if args.rank_of == 1 else shard.unknowns
     nid = None
     if ws > 1:
         obj = [pk.nccl_unique_id() if rank == 0 else None]
@@ -430,7 +436,7 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": prob.unknowns / (float(te[0]) * 1e-3), "unit": "unknowns/s",
+        e2e = {"value": job_unknowns / (float(te[0]) * 1e-3), "unit": "unknowns/s",
                "ms_per_step": float(te[0]), "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": 8 * sw.out_size}
 
     parity = None
@@ -442,7 +448,7 @@ def main():
         gb = min(32, 1 << max(0, (shard.G - 1).bit_length()))
         f_edg = flops_per_edg(prob.p, prob.dim, nd // (4 if prob.dim == 2 else 2), gb) + \
             option_flops_per_edg(prob.p, prob.dim, opts)
-        flops = f_edg * prob.n_el * nd * prob.G / ws          # per rank per launch (folded)
+        flops = f_edg * prob.n_el * nd * (g1 - g0)             # per rank per launch (folded)
         achieved_tf = flops / (sweep_ms * 1e-3) / 1e12
         peak_nominal = SMS * FP64_FMA_PER_SM_CLK * 2 * SM_MAX_MHZ * 1e6 / 1e12
         peaks = measured_peaks()
@@ -453,7 +459,7 @@ def main():
             peak_probe = None
         rec = {
             "metric": METRIC,
-            "value": prob.unknowns / (step_ms * 1e-3),
+            "value": job_unknowns / (step_ms * 1e-3),
             "unit": "unknowns/s",
             "n_gpus": ws,
             "steps": args.steps,
@@ -466,8 +472,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config] + (f" + options {sorted(opts)}" if opts else ""),
                        "fold_z": True, "distinct_directions": nd,
-                       "unknowns": prob.unknowns, "groups_per_rank": g1 - g0,
-                       "parallelism": f"group-sharded x{ws}" + (" + NCCL all-reduce" if ws > 1 else ""),
+                       "unknowns": job_unknowns, "groups_per_rank": g1 - g0,
+                       "parallelism": (f"group-sharded x{ws}" + (" + NCCL all-reduce" if ws > 1 else "")) if args.rank_of == 1
+                       else f"per-rank workload of a {args.rank_of}-way group split (rank 0, one GPU, no all-reduce)",
                        "l2": ("inputs %.2f GB > 126 MB L2, no flush" % (in_bytes / 1e9)) if not flush.numel()
                        else "1 GiB L2 flush before every step (outside the step's events)"},
             "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_nominal, "unit": "TFLOP/s",
