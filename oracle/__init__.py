@@ -11,7 +11,12 @@ exactness, global particle balance, convergence order, rotation symmetry,
 quadrature identities; sigma-weighted moments pinned by their reductions
 (one group, group-constant sigma, constant solution); the fixup pinned by
 the worked element examples and an independent element-by-element sweep in
-the jump/average form (tests/dense_dg.py) on tiny meshes.
+the jump/average form (tests/dense_dg.py) on tiny meshes; the half-range moments
+by an independent psi and isotropic closed forms; the TRT step by the Planck
+series, Stefan-Boltzmann, the elimination's fixed point, a brute-force nodal
+Newton on the dense global solve, and its outer stop rule (eq:relative_tol) by
+rebuilding the iterate sequence from fixed-iteration runs
+(tests/test_oracle_next.py::test_trt_stop_rule_rebuilt).
 """
 from __future__ import annotations
 

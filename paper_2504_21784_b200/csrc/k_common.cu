@@ -230,8 +230,7 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
     const bool defer = SWEEP_DEFER_C && !(k == 1 && gbk == 1);
     const int s2 = ((opt & OPT_SIGMA) || defer) ? CT * (dset * NQ + 1) : 0;
     const int rc = 2 * ((k * (p + 1) + 1) / 2);  // trace-ring record per lane (pairs of doubles)
-    const int lsm = (SWEEP_LANE_SMEM && p == 2) ? 18 * dset : 0;  // experiment: per-direction solve constants
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + ((dset * 16 + 1) & ~1) + rc * NL + 81 + s2 + lsm) *
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + ((dset * 16 + 1) & ~1) + rc * NL + 81 + s2) *
            (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }

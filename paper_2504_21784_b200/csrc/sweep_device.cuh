@@ -208,7 +208,6 @@ __device__ __forceinline__ LaneP2 make_lane_p2(double cx, double cy, double kap 
 }
 
 __device__ __forceinline__ void traces_p2(const double (&u)[9], double (&txo)[3], double (&tyo)[3]);
-__device__ __forceinline__ double rcp64_fast(double x);
 
 // modal element solve: u = (sigma~ + cx lam_a + cy lam_b)^-1 (q^ + lifts), and the
 // outflow traces in modal form (x+ face: y-modal, y+ face: x-modal).
@@ -250,57 +249,6 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     u[6] = (r11i * e11 - r11r * L.I11) * i11;
     u[7] = (r12r * e11 + r12i * L.I12) * i12;
     u[8] = (r12i * e11 - r12r * L.I12) * i12;
-    traces_p2(u, txo, tyo);
-}
-
-#ifndef SWEEP_LANE_SMEM
-#define SWEEP_LANE_SMEM 0  // experiment: per-direction solve constants read from shared memory per use
-#endif
-// the per-direction constants of solve_p2 read from shared memory at each use (volatile: no
-// hoisting into registers), to free the 36 registers a LaneP2 occupies
-__device__ __forceinline__ double lds_v(const double* p) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
-    return v;
-}
-__device__ __forceinline__ void solve_p2_smem(const LaneP2* Lp, double st, const double (&qh)[9], const double (&tx)[3],
-                                              const double (&ty)[3], double (&u)[9], double (&txo)[3], double (&tyo)[3]) {
-    const double* Lf = reinterpret_cast<const double*>(Lp);
-    auto F = [&](int i) { return lds_v(Lf + i); };
-    // field order of LaneP2: lx0 lx1r lx1i ly0 ly1r ly1i A00 A01 A10 A11 I01 I10 I11 I12 I01s I10s I11s I12s
-    const double r00 = qh[0] + F(0) * tx[0] + F(3) * ty[0];
-    const double r01r = qh[1] + F(0) * tx[1] + F(4) * ty[0];
-    const double r01i = qh[2] + F(0) * tx[2] + F(5) * ty[0];
-    const double r10r = qh[3] + F(1) * tx[0] + F(3) * ty[1];
-    const double r10i = qh[4] + F(2) * tx[0] + F(3) * ty[2];
-    const double r11r = qh[5] + F(1) * tx[1] - F(2) * tx[2] + F(4) * ty[1] - F(5) * ty[2];
-    const double r11i = qh[6] + F(1) * tx[2] + F(2) * tx[1] + F(4) * ty[2] + F(5) * ty[1];
-    const double r12r = qh[7] + F(1) * tx[1] + F(2) * tx[2] + F(4) * ty[1] + F(5) * ty[2];
-    const double r12i = qh[8] + F(2) * tx[1] - F(1) * tx[2] + F(4) * ty[2] - F(5) * ty[1];
-    const double I01 = F(10), I10 = F(11), I11 = F(12), I12 = F(13);
-    const double d00 = st + F(6);
-    const double e01 = st + F(7), m01 = fma(e01, e01, F(14));
-    const double e10 = st + F(8), m10 = fma(e10, e10, F(15));
-    const double e11 = st + F(9);
-    const double e11s = e11 * e11;
-    const double m11 = e11s + F(16), m12 = e11s + F(17);
-    const double pa = d00 * m01, pb = m10 * m11;
-    const double pab = pa * pb, p4 = pab * m12;
-    const double inv = rcp64_fast(p4);
-    const double i12 = inv * pab;
-    const double iab = inv * m12;
-    const double ia = iab * pb, ib = iab * pa;
-    const double i00 = ia * m01, i01 = ia * d00;
-    const double i10 = ib * m11, i11 = ib * m10;
-    u[0] = r00 * i00;
-    u[1] = (r01r * e01 + r01i * I01) * i01;
-    u[2] = (r01i * e01 - r01r * I01) * i01;
-    u[3] = (r10r * e10 + r10i * I10) * i10;
-    u[4] = (r10i * e10 - r10r * I10) * i10;
-    u[5] = (r11r * e11 + r11i * I11) * i11;
-    u[6] = (r11i * e11 - r11r * I11) * i11;
-    u[7] = (r12r * e11 + r12i * I12) * i12;
-    u[8] = (r12i * e11 - r12r * I12) * i12;
     traces_p2(u, txo, tyo);
 }
 
@@ -753,10 +701,6 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         // limit) and not for one group per direction (C3: 0.324 -> 0.347 ms)
         constexpr bool DEFER = SWEEP_DEFER_C && !SIG && !(K == 1 && LG == 1);
         double* Salt = S2 + (SIG ? (size_t)CT * SEL : 0);  // DEFER: S of the odd chunks
-        LaneP2* Lsm = reinterpret_cast<LaneP2*>(Salt + (DEFER ? (size_t)CT * SEL : 0));  // SWEEP_LANE_SMEM: [dset]
-        if constexpr (P == 2 && SWEEP_LANE_SMEM) {
-            if (gl == 0 && d_on) Lsm[dl] = make_lane_p2(cx, cy, SIG ? prm.inv_c_dt : 0.0);
-        }
         const size_t sig_off = 6 * nodes + 2 * (size_t)prm.nbnode;  // SIG: sigma phi | sigma J
         // (compile-time constant-bank indices only: ptxas hoists constant loads out of
         // the task loop for every thread, and a thread-dependent index past the end of
@@ -1322,8 +1266,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                         for (int m = 0; m < NQ; ++m) qh[m] = qs[((size_t)el * NN + m) * GBK + gl + k * LG];
                         const double st = ss[el * GBK + gl + k * LG];
-                        if constexpr (P == 2 && SWEEP_LANE_SMEM) solve_p2_smem(Lsm + dl, st, qh, tx[k][r], ty[k], u, txo, tyo);
-                        else if constexpr (P == 2) solve_p2(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
+                        if constexpr (P == 2) solve_p2(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
                         else solve_p1(L, st, qh, tx[k][r], ty[k], u, txo, tyo);
                         if constexpr (FIX) {
                             if constexpr (P == 2) {
