@@ -1253,7 +1253,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                 // p = 1 without options: the group sums of the column's T elements are kept and
                 // reduced across the lanes of a direction together after the column (one
                 // reduce-scatter of T*NQ values: fewer shuffles, and off the row-to-row chain)
-                constexpr bool BATCH = (P == 1) && !SIG && LG > 1;
+#ifndef SWEEP_BATCH_P2
+#define SWEEP_BATCH_P2 0  // experiment: the column-batched reduction for p = 2 as well
+#endif
+                constexpr bool BATCH = (P == 1 || SWEEP_BATCH_P2) && !SIG && !FIX && LG > 1;
                 double usc[BATCH ? T * NQ : 1];
 #pragma unroll
                 for (int r = 0; r < T; ++r) {

@@ -137,6 +137,17 @@ def test_config5_full_size_replicated_groups(lib):
     assert_parity(got, ref, 2, 512, 512, 2)
 
 
+def test_config5_full_all_groups(lib):
+    """C5 exactly as BASELINE.json states it and bench.py launches it — 512^2, p = 2, 128
+    directions, all 64 distinct groups — against the oracle on every output (the oracle sweeps
+    the 64 groups on the host's cores: about 2.5 min on 16 cores)."""
+    prob = synth.config(5)
+    got = gpu_out(lib, prob)
+    ref = oracle.sweep(prob)
+    errs = assert_parity(got, ref, 2, 512, 512, 2)
+    assert max(e for e, _ in errs.values()) <= 1e-11
+
+
 # ------------------------------------------------------------------ properties at full size
 def _constant_problem(prob, Q=1.3):
     q = np.ascontiguousarray(np.broadcast_to(((prob.sigma + prob.inv_c_dt) * Q)[:, None, :], prob.q.shape))
