@@ -1250,13 +1250,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                         cp_async_commit();
                     }
                 }
-                // p = 1 without options: the group sums of the column's T elements are kept and
-                // reduced across the lanes of a direction together after the column (one
-                // reduce-scatter of T*NQ values: fewer shuffles, and off the row-to-row chain)
-#ifndef SWEEP_BATCH_P2
-#define SWEEP_BATCH_P2 0  // experiment: the column-batched reduction for p = 2 as well
-#endif
-                constexpr bool BATCH = (P == 1 || SWEEP_BATCH_P2) && !SIG && !FIX && LG > 1;
+                // without sigma moments / fixup: the group sums of the column's T elements are
+                // kept and reduced across the lanes of a direction together after the column
+                // (one reduce-scatter of T*NQ values: fewer shuffles, and off the row-to-row
+                // chain).  C4 1.00 -> 0.88 ms; C5 10.82 -> 10.50 ms, 8-group rank 3.34 -> 3.09 ms
+                constexpr bool BATCH = !SIG && !FIX && LG > 1;
                 double usc[BATCH ? T * NQ : 1];
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
