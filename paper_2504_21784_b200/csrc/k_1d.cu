@@ -29,13 +29,12 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
     constexpr int NM = SIG ? 5 : 3;                  // phi, J, Txx (+ sigma phi, sigma J)
     constexpr int NV = (NM + (HALF ? 1 : 0)) * NP1;  // (+ P_xx)
     constexpr int D = 8;                             // prefetch distance (elements): ~HBM latency / step
-    constexpr int SB = (NV <= 8) ? 4 : 2;            // steps per chain-sum barrier (shared memory: 2 SB slots)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int W = blockDim.x >> 5;
     const int nx = prm.nx, G = prm.G, L = prm.seglen;
     const size_t nodes = prm.nodes;
-    extern __shared__ __align__(16) double red[];    // [2 SB][W][32][NV] + [W][4] (+ single: [NM][nodes])
-    double* bred = red + 2 * SB * (size_t)W * 32 * NV;
+    extern __shared__ __align__(16) double red[];    // [2][W][32][NV] + [W][4] (+ single: [NM][nodes])
+    double* bred = red + 2 * (size_t)W * 32 * NV;
     double* acc1 = bred + 4 * (size_t)W;             // single: the gray fields of the whole mesh
 
     // this warp's chain.  Slab mode: the CTA's chains are one half-range's [g0, g0 + ng).
@@ -160,30 +159,18 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
 #pragma unroll
             for (int k = 0; k < NV; ++k) v[k] = 0.0;
         }
-        // this step's values into slot t % (2 SB); every SB steps (and after the last) one
-        // barrier, then the CTA sums the SB buffered steps (double-buffered slot halves)
-        // (single mode: a barrier every step — two items of one block could be the two halves'
-        // contributions to the same element)
-        const int sb = single ? 1 : SB;
-        double* rb = red + ((size_t)(t % (2 * sb)) * W + w) * 32 * NV + lane * NV;
+        double* rb = red + ((size_t)(t & 1) * W + w) * 32 * NV + lane * NV;
 #pragma unroll
         for (int k = 0; k < NV; ++k) rb[k] = v[k];
-        if ((t + 1) % sb != 0 && t + 1 < L) {
-            ++t;
-            return;
-        }
         __syncthreads();
-        const int tb0 = t - (t % sb);  // first step of this block
-        const int nb = t - tb0 + 1;
-        // sum over the CTA's chains (warp order) for the 32 elements of each buffered step
+        // sum over the CTA's chains (warp order) for the 32 elements of this step
+        const double* rs = red + (size_t)(t & 1) * W * 32 * NV;
         if (single) {
             // per half-range (its own physical element at this step), added to the mesh fields;
             // one thread per (segment, value) handles both halves: no two threads share an entry
-            for (int o = tid; o < nb * 32 * NV; o += blockDim.x) {
-                const int tt = tb0 + o / (32 * NV), so = o % (32 * NV);
-                const int s = so / NV, r = so - s * NV;
-                const double* rs = red + (size_t)(tt % (2 * sb)) * W * 32 * NV;
-                const int ips = s * L + tt;
+            for (int o = tid; o < 32 * NV; o += blockDim.x) {
+                const int s = o / NV, r = o - s * NV;
+                const int ips = s * L + t;
                 if (ips >= min(nx, (s + 1) * L)) continue;
                 const int m = r / NP1, aq = r - m * NP1;
 #pragma unroll
@@ -200,11 +187,9 @@ __global__ void __launch_bounds__(256) sweep1d_scan_kernel(const Sweep1DScanPara
             ++t;
             return;
         }
-        for (int o = tid; o < nb * 32 * NV; o += blockDim.x) {
-            const int tt = tb0 + o / (32 * NV), so = o % (32 * NV);
-            const int s = so / NV, r = so - s * NV;
-            const double* rs = red + (size_t)(tt % (2 * sb)) * W * 32 * NV;
-            const int ips = s * L + tt;
+        for (int o = tid; o < 32 * NV; o += blockDim.x) {
+            const int s = o / NV, r = o - s * NV;
+            const int ips = s * L + t;
             if (ips >= min(nx, (s + 1) * L)) continue;
             double acc = 0.0;
             for (int ww = 0; ww < W; ++ww) acc += rs[((size_t)ww * 32 + s) * NV + r];
@@ -279,8 +264,7 @@ static const void* pick_scan(int opt) {
 int scan1d_smem_bytes(int p, int opt, int warps, size_t single_nodes) {
     const int nm = (opt & OPT_SIGMA) ? 5 : 3;
     const int nv = (nm + ((opt & OPT_HALF) ? 1 : 0)) * (p + 1);
-    const int sb = (nv <= 8) ? 4 : 2;  // as SB in the kernel
-    return (int)(sizeof(double) * (2 * sb * (size_t)warps * 32 * nv + warps * 4 + (size_t)nm * single_nodes));
+    return (int)(sizeof(double) * (2 * (size_t)warps * 32 * nv + warps * 4 + (size_t)nm * single_nodes));
 }
 
 int launch_sweep1d_scan(int p, int opt, const Sweep1DScanParams& prm, int grid, int block, size_t smem, void* stream) {
