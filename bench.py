@@ -271,6 +271,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-floors", action="store_true", help="skip the launch-floor and graph-replay probes "
+                                                              "(keeps an ncu launch list to the step's kernels)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--rank-of", type=int, default=1,
                     help="analysis: on one GPU, sweep only the group shard rank 0 of a K-rank group split owns "
@@ -406,7 +408,7 @@ def main():
     # latency floors (C1-C3 are reported against them): an empty kernel launch,
     # and the same step replayed from a CUDA graph
     floors = None
-    if "trt" not in opts:
+    if "trt" not in opts and not args.no_floors:
         try:
             floors = {"empty_launch_us": pk.launch_floor(local),
                       "graph_replay_ms": graph_replay_ms(sw, lambda: sw.sweep_run(sig, prob.inv_c_dt, q, fl), stream),

@@ -7,7 +7,7 @@ for o in sigma fixup halfrange trt; do python bench.py --no-cpu --no-e2e --no-pa
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
 timeout 1500 python scripts/stress_parity.py 20000 31 > gpurun_out/stress20k.txt 2>&1; echo stress=$?
 timeout 600 python scripts/shard_perf.py 8,16,32 "" 8 > gpurun_out/shard.txt 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity > gpurun_out/ncu_l.log 2>&1; echo ncul=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity --no-floors > gpurun_out/ncu_l.log 2>&1; echo ncul=$?
 ncu --set full --clock-control none --import-source on -k regex:sweep2d_kernel -s 3 -c 1 -o gpurun_out/sweep2d_c5_final python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > gpurun_out/ncu_full.log 2>&1; echo ncufull=$?
 ncu --set full --clock-control none --import-source on -k regex:sweep2d_kernel -s 3 -c 1 -o gpurun_out/sweep2d_c4_final python bench.py --config 4 --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > gpurun_out/ncu_c4.log 2>&1; echo ncuc4=$?
 for v in hint pa4; do timeout 300 python scripts/fault_repro.py build/$v.so > gpurun_out/fault_$v.txt 2>&1; echo fault_$v=$?; done
