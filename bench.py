@@ -414,6 +414,8 @@ def main():
                       "graph_replay_ms": graph_replay_ms(sw, lambda: sw.sweep_run(sig, prob.inv_c_dt, q, fl), stream),
                       "launches_per_step": launches_per_step}
             floors["step_floor_ms"] = floors["empty_launch_us"] * launches_per_step * 1e-3
+            # the step's device time (graph replay) in units of the empty-launch floor
+            floors["graph_replay_over_floor"] = floors["graph_replay_ms"] / floors["step_floor_ms"]
         except Exception as ex:  # noqa: BLE001
             floors = {"error": str(ex)[:200]}
 
