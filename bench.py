@@ -44,7 +44,9 @@ def flops_per_edg(p: int, dim: int, n_dir_quad: int, gb: int) -> float:
     """Flops per (element, distinct direction, group) of the implemented algorithm
     (FMA = 2, reciprocal = 1), counted from the kernel source."""
     if dim == 2 and p == 2:
-        solve = 52 + 11 + 13 + 33 + 11           # lifts, shifts, reciprocals, scaling, traces
+        # lifts (40 since round 2: the (1,1)/(1,2) pair lifted as half sum and difference,
+        # 8 FMA + 4 adds instead of 16 FMA), shifts, reciprocals, scaling, traces
+        solve = 40 + 11 + 13 + 33 + 11
         group_sum = 9                             # sum over groups of the 9 modal values
         q_transform = 2 * 81 / n_dir_quad         # modal transform of q per (e, g), per quadrant
         moments = 2 * (6 * 9 + 6 * 81 / n_dir_quad) / gb
@@ -500,6 +502,7 @@ def main():
                                                stats["ctas"] * stats["block"] * stats["groups_per_lane"]),
             "parity": parity,
             "clocks": clk,
+            "layout": {k: int(v) for k, v in stats.items()},
             "step_breakdown_ms": {"sweep": float(kt[:, 0].mean()), "finalize": float(kt[:, 1].mean()),
                                   "allreduce": float(kt[:, 2].mean())},
         }

@@ -235,6 +235,7 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }
 int sweep2d_cols_per_chunk(int p, int k, int opt) { return cols_per_chunk(p, k, opt); }
+int sweep2d_ring_record(int p, int k, int log2lg, int opt) { return ring_record(p, k, 1 << log2lg, opt); }
 
 // The dynamic shared-memory cap is one value per kernel for the whole process, so it is
 // always raised to the device's opt-in maximum (never to one handle's size: a smaller
@@ -443,7 +444,7 @@ __global__ void selfcheck_solves_kernel(int n, unsigned long long seed, unsigned
     } else {
         const LaneP2 L = make_lane_p2(cx, cy);
         double qh[9], txm[3], tym[3], u[9], txo[3], tyo[3];
-        modal_forward(q, qh);
+        modal_forward_sd(q, qh);
         txm[0] = cM.W0[0] * tx[0] + cM.W0[1] * tx[1] + cM.W0[2] * tx[2];
         txm[1] = cM.W1re[0] * tx[0] + cM.W1re[1] * tx[1] + cM.W1re[2] * tx[2];
         txm[2] = cM.W1im[0] * tx[0] + cM.W1im[1] * tx[1] + cM.W1im[2] * tx[2];

@@ -131,6 +131,19 @@ __device__ __forceinline__ void ld_pair_cg(const double* p, double& a, double& b
 __device__ __forceinline__ void st_pair(double* p, double a, double b) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
+// Strip-boundary traces with a data-carried tag (the LL line format of NCCL's low-latency
+// protocol): a double travels as one 16-byte store {lo, tag, hi, tag}, and a reader that sees
+// both 8-byte halves carry the expected tag has the whole value -- no release fence, no flag.
+__device__ __forceinline__ void ll_store(double* p, double v, unsigned tag) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)__double2loint(v)),
+                 "r"(tag), "r"((unsigned)__double2hiint(v)), "r"(tag)
+                 : "memory");
+}
+__device__ __forceinline__ void ll_load(const double* p, unsigned (&w)[4]) {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -211,6 +224,11 @@ __device__ __forceinline__ void traces_p2(const double (&u)[9], double (&txo)[3]
 
 // modal element solve: u = (sigma~ + cx lam_a + cy lam_b)^-1 (q^ + lifts), and the
 // outflow traces in modal form (x+ face: y-modal, y+ face: x-modal).
+// qh is the STAGED source (modal_forward_sd): slots 5..8 hold the half sum and half
+// difference of the (1,1) and (1,2) modes, s = (q11 + q12)/2, d = (q11 - q12)/2.  The lifts
+// of both traces reach those modes as lx1 t1 + ly1 ty1 and lx1 conj(t1) + conj(ly1) ty1, whose
+// half sum lx1 Re(t1) + ly1r ty1 and half difference i (lx1 Im(t1) + ly1i ty1) take 8 FMAs;
+// r11 = s + d, r12 = s - d then cost 4 adds (16 FMAs to form r11, r12 directly).
 __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const double (&qh)[9], const double (&tx)[3],
                                          const double (&ty)[3], double (&u)[9], double (&txo)[3], double (&tyo)[3]) {
     const double r00 = qh[0] + L.lx0 * tx[0] + L.ly0 * ty[0];
@@ -218,10 +236,12 @@ __device__ __forceinline__ void solve_p2(const LaneP2& L, double st, const doubl
     const double r01i = qh[2] + L.lx0 * tx[2] + L.ly1i * ty[0];
     const double r10r = qh[3] + L.lx1r * tx[0] + L.ly0 * ty[1];
     const double r10i = qh[4] + L.lx1i * tx[0] + L.ly0 * ty[2];
-    const double r11r = qh[5] + L.lx1r * tx[1] - L.lx1i * tx[2] + L.ly1r * ty[1] - L.ly1i * ty[2];
-    const double r11i = qh[6] + L.lx1r * tx[2] + L.lx1i * tx[1] + L.ly1r * ty[2] + L.ly1i * ty[1];
-    const double r12r = qh[7] + L.lx1r * tx[1] + L.lx1i * tx[2] + L.ly1r * ty[1] + L.ly1i * ty[2];
-    const double r12i = qh[8] + L.lx1i * tx[1] - L.lx1r * tx[2] + L.ly1r * ty[2] - L.ly1i * ty[1];
+    const double sr = qh[5] + L.lx1r * tx[1] + L.ly1r * ty[1];
+    const double si = qh[6] + L.lx1i * tx[1] + L.ly1r * ty[2];
+    const double dr = qh[7] - L.lx1i * tx[2] - L.ly1i * ty[2];
+    const double di = qh[8] + L.lx1r * tx[2] + L.ly1i * ty[1];
+    const double r11r = sr + dr, r11i = si + di;
+    const double r12r = sr - dr, r12i = si - di;
 
     const double d00 = st + L.A00;
     const double e01 = st + L.A01, m01 = fma(e01, e01, L.I01s);
@@ -288,6 +308,26 @@ __device__ __forceinline__ void modal_forward(const double (&q)[9], double (&qh)
     qh[6] = ri + ir;
     qh[7] = rr + ii;   // (1,2) = sum W1 conj(W1)
     qh[8] = ri - ir;
+}
+// the staged source of solve_p2: modal_forward with the (1,1), (1,2) pair as its half sum
+// (rr, ri) and half difference (-ii, ir)
+__device__ __forceinline__ void modal_forward_sd(const double (&q)[9], double (&qh)[9]) {
+    double s0[3], s1r[3], s1i[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        s0[b] = cM.W0[0] * q[3 * b] + cM.W0[1] * q[3 * b + 1] + cM.W0[2] * q[3 * b + 2];
+        s1r[b] = cM.W1re[0] * q[3 * b] + cM.W1re[1] * q[3 * b + 1] + cM.W1re[2] * q[3 * b + 2];
+        s1i[b] = cM.W1im[0] * q[3 * b] + cM.W1im[1] * q[3 * b + 1] + cM.W1im[2] * q[3 * b + 2];
+    }
+    qh[0] = cM.W0[0] * s0[0] + cM.W0[1] * s0[1] + cM.W0[2] * s0[2];
+    qh[1] = cM.W1re[0] * s0[0] + cM.W1re[1] * s0[1] + cM.W1re[2] * s0[2];
+    qh[2] = cM.W1im[0] * s0[0] + cM.W1im[1] * s0[1] + cM.W1im[2] * s0[2];
+    qh[3] = cM.W0[0] * s1r[0] + cM.W0[1] * s1r[1] + cM.W0[2] * s1r[2];
+    qh[4] = cM.W0[0] * s1i[0] + cM.W0[1] * s1i[1] + cM.W0[2] * s1i[2];
+    qh[5] = cM.W1re[0] * s1r[0] + cM.W1re[1] * s1r[1] + cM.W1re[2] * s1r[2];      // rr
+    qh[6] = cM.W1re[0] * s1i[0] + cM.W1re[1] * s1i[1] + cM.W1re[2] * s1i[2];      // ri
+    qh[7] = -(cM.W1im[0] * s1i[0] + cM.W1im[1] * s1i[1] + cM.W1im[2] * s1i[2]);   // -ii
+    qh[8] = cM.W1im[0] * s1r[0] + cM.W1im[1] * s1r[1] + cM.W1im[2] * s1r[2];      // ir
 }
 
 // ---- zero-and-scale negative flux fixup:
@@ -422,6 +462,23 @@ __host__ __device__ constexpr int cols_per_chunk(int P, int K, int OPT = 0) {
 }
 // (K = 2: T = 4 rows, C = 4 columns -> 16 elements per chunk, like K = 4)
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
+// Strip hand-off protocol: K <= 2 groups per lane with a group reduction (the column loop:
+// C4, the small group-sharded ranks) pass the y-traces as tagged LL lines, column by column
+// (the strip above may run one column behind the strip below); otherwise per-chunk progress
+// flags (release / acquire) and plain 16-byte pair records.
+#ifndef SWEEP_LL
+#define SWEEP_LL 1
+#endif
+#ifndef SWEEP_LL_KMAX
+#define SWEEP_LL_KMAX 2
+#endif
+__host__ __device__ constexpr bool ll_ring(int P, int K, int LG, int OPT) {
+    return SWEEP_LL && K <= SWEEP_LL_KMAX && !(K == 1 && LG == 1 && !(OPT & OPT_FIXUP)) && P >= 1;
+}
+// doubles per lane and column in the trace ring
+__host__ __device__ constexpr int ring_record(int P, int K, int LG, int OPT) {
+    return ll_ring(P, K, LG, OPT) ? 2 * K * (P + 1) : 2 * ((K * (P + 1) + 1) / 2);
+}
 
 __device__ __forceinline__ int bnode2d(int face, int idx, int node, int nx, int ny, int np1) {
     switch (face) {
@@ -555,7 +612,10 @@ template <int P, int LOG2LG, int K, int OPT>
 #ifndef SWEEP_K1_MINB
 #define SWEEP_K1_MINB 1
 #endif
-__global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1))) sweep2d_kernel(const Sweep2DParams prm) {
+#ifndef SWEEP_K1_MAXT
+#define SWEEP_K1_MAXT 256  // experiment builds: 128 with SWEEP_K1_MINB 3-4 (one-group-per-lane p = 2 ranks)
+#endif
+__global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1))) sweep2d_kernel(const Sweep2DParams prm) {
     constexpr bool SIG = (OPT & OPT_SIGMA) != 0;
     constexpr bool FIX = (OPT & OPT_FIXUP) != 0;
     constexpr int NP1 = P + 1;
@@ -571,6 +631,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
     // strip-boundary trace ring: per column, each lane's K*NT trace reals as KT2 pairs, laid
     // out [pair][lane][2] (16-byte vector stores / loads / cp.async, coalesced per warp)
     constexpr int KT = K * NT, KT2 = (KT + 1) / 2, RC = 2 * KT2;
+    constexpr bool LL = ll_ring(P, K, LG, OPT);
+    constexpr int RL = ring_record(P, K, LG, OPT);  // ring doubles per lane and column
 
     const int NL = blockDim.x;
     const int tid = threadIdx.x;
@@ -595,10 +657,19 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         fence_proxy_async();
     }
     unsigned phase_bits = 0;  // parity of the next completion of mbar[0] (bit 0) and mbar[1] (bit 1)
+    // LL ring tags of this launch: (epoch + 1) << 16 | strip -- a line read by strip J + 1 was
+    // written in this launch (never zero; an earlier launch's tag repeats after 32768 launches,
+    // by which time every line it wrote has been rewritten)
+    const unsigned ll_tag = LL ? (((unsigned)ld_relaxed_gpu(prm.epoch) & 0x7fffu) + 1u) << 16 : 0u;
     const unsigned long long pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
     for (;;) {
-        if (tid == 0) s_task = atomicAdd(prm.task_counter, 1);
+        if (tid == 0) {
+            s_task = atomicAdd(prm.task_counter, 1);
+            // the CTA with the last claim of all: every CTA has finished (and read the epoch at
+            // its start), so the next launch may use the next tag
+            if (s_task == prm.n_tasks + (int)gridDim.x - 1) atomicAdd(prm.epoch, 1);
+        }
         __syncthreads();
         const int task = s_task;
         __syncthreads();
@@ -618,8 +689,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             cx = prm.dirs[sd.d0 + dl].cx;
             cy = prm.dirs[sd.d0 + dl].cy;
         }
-        const int j0 = J * T;
-        const int rows = min(T, ny - j0);
+        // balanced strips (host): strip_a strips of row_hi rows, then strips of row_lo rows
+        const int j0 = (J < prm.strip_a) ? J * prm.row_hi : prm.strip_a * prm.row_hi + (J - prm.strip_a) * prm.row_lo;
+        const int rows = min((J < prm.strip_a) ? prm.row_hi : prm.row_lo, ny - j0);
         double* slab = prm.slabs + (size_t)s * prm.out_size;
         const bool bulk = prm.bulk_ok && ((sd.ng & 1) == 0) && ((sd.g0 & 1) == 0);
 
@@ -721,6 +793,18 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
         }
 
         bool y0_pref = false;  // J == 0: ypre holds the next column's raw y-inflow
+        // LL ring: this task's tags, and the tagged lines of the next column this lane reads
+        // (loaded one column ahead; re-read until the tags match)
+        const unsigned tag_out = ll_tag | (unsigned)J, tag_in = ll_tag | (unsigned)(J - 1);
+        const double* ll_src = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * prm.nx_pad * (size_t)RL * blockDim.x;
+        unsigned llv[LL ? KT : 1][4];
+        int llv_col = -1;
+        auto ll_fetch = [&](const int ipc) {
+#pragma unroll
+            for (int t = 0; t < (LL ? KT : 1); ++t) ll_load(ll_src + (((size_t)ipc * KT + t) * NL + tid) * 2, llv[t]);
+            llv_col = ipc;
+        };
+        if (LL && J > 0) ll_fetch(0);
         // x-inflow traces of the strip (domain boundary at i' = 0)
         double tx[K][T][NT];
 #pragma unroll
@@ -976,7 +1060,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     ss[el * GBK + gg] = st[u];
                     if constexpr (P == 2) {
                         double qh[9];
-                        modal_forward(qv[u], qh);
+                        modal_forward_sd(qv[u], qh);
 #pragma unroll
                         for (int m = 0; m < 9; ++m) qs[((size_t)el * NN + m) * GBK + gg] = qh[m];
                     } else {
@@ -990,7 +1074,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                 if (c > 0) phase_c(i0 - C, C, ((c - 1) & 1) ? Salt : S);
             // ---- wait until the strip below has finished this chunk
 #ifndef SWEEP_ABL_NOWAIT
-            if (J > 0 && tid == 0) {
+            if (!LL && J > 0 && tid == 0) {
 #else
             if (false) {
 #endif
@@ -1041,8 +1125,8 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
             if constexpr (P == 2) L = make_lane_p2(cx, cy, kap);
             else L = make_lane_p1(cx, cy, kap);
             const int nxp = prm.nx_pad;
-            const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)RC * NL;
-            double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)RC * NL;
+            const double* ysrc = prm.ytr + ((size_t)s * 2 + ((J + 1) & 1)) * nxp * (size_t)RL * NL;
+            double* ydst = prm.ytr + ((size_t)s * 2 + (J & 1)) * nxp * (size_t)RL * NL;
             const bool write_y = J + 1 < prm.n_strips;
 #ifndef SWEEP_COL_UNROLL
 #define SWEEP_COL_UNROLL 1
@@ -1222,11 +1306,34 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     // (issued after this chunk's acquire), later columns from the private
                     // shared-memory slots the previous column prefetched with cp.async
 #ifdef SWEEP_DEBUG
-                    SWEEP_DCHECK(ysrc + ((size_t)ip + 1) * RC * NL <= prm.ytr + prm.ring_len);
-                    SWEEP_DCHECK(__ldcg(prm.ytag + ((size_t)s * 2 + ((J + 1) & 1)) * nxp + ip) == J - 1);
+                    SWEEP_DCHECK(ysrc + ((size_t)ip + 1) * RL * NL <= prm.ytr + prm.ring_len);
+                    if (!LL) SWEEP_DCHECK(__ldcg(prm.ytag + ((size_t)s * 2 + ((J + 1) & 1)) * nxp + ip) == J - 1);
 #endif
                     double yt[RC];
-                    if (col == 0) {
+                    if constexpr (LL) {
+                        // the lines fetched one column ago, re-read until both halves of every
+                        // line carry the tag of strip J - 1 (watchdog: a writer that never
+                        // arrives must not hang the GPU)
+                        auto ready = [&]() {
+                            bool ok = llv_col == ip;
+#pragma unroll
+                            for (int t = 0; t < KT; ++t) ok = ok && llv[t][1] == tag_in && llv[t][3] == tag_in;
+                            return ok;
+                        };
+                        if (!ready()) {
+                            const long long t_start = clock64();
+                            do {
+                                ll_fetch(ip);
+                                // a timed-out wait anywhere (error bit 4) ends every other wait
+                                if (clock64() - t_start > (1LL << 34) || (ld_relaxed_gpu(prm.err) & 4)) {
+                                    atomicOr(prm.err, 4);
+                                    break;
+                                }
+                            } while (!ready());
+                        }
+#pragma unroll
+                        for (int t = 0; t < KT; ++t) yt[t] = __hiloint2double((int)llv[t][2], (int)llv[t][0]);
+                    } else if (col == 0) {
 #pragma unroll
                         for (int pi = 0; pi < KT2; ++pi)
                             ld_pair_cg(ysrc + (((size_t)ip * KT2 + pi) * NL + tid) * 2, yt[2 * pi], yt[2 * pi + 1]);
@@ -1243,7 +1350,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
                     for (int k = 0; k < K; ++k)
 #pragma unroll
                         for (int t = 0; t < NT; ++t) ty[k][t] = yt[k * NT + t];
-                    if (col + 1 < C) {
+                    if (!LL && col + 1 < C) {
 #pragma unroll
                         for (int pi = 0; pi < KT2; ++pi)
                             cp_async16(ypre + ((size_t)pi * NL + tid) * 2, ysrc + (((size_t)(ip + 1) * KT2 + pi) * NL + tid) * 2);
@@ -1259,6 +1366,15 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
                     const int el = col * T + r;
+                    if (r >= rows) {
+                        // a short strip (balanced heights): no element; the y-trace passes on
+                        // from the strip's top row
+                        if constexpr (BATCH) {
+#pragma unroll
+                            for (int m = 0; m < NQ; ++m) usc[r * NQ + m] = 0.0;
+                        }
+                        continue;
+                    }
                     // us: group sum of the modal solution; SIG also the sigma-weighted sum
                     double us[SIG ? 2 * NQ : NQ];
 #pragma unroll
@@ -1314,14 +1430,6 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #endif
                     }
                 }
-                if constexpr (BATCH) {
-                    // element r of this column: values [r NQ, (r+1) NQ) of usc
-                    auto sink = [&](int idx, double val) {
-                        const int r = idx / NQ;
-                        Sc[(size_t)(col * T + r) * SEL + dl * NQ + (idx - r * NQ)] = val;
-                    };
-                    ReduceScatter<T * NQ, LG / 2>::run(usc, lane, 0, T * NQ, sink);
-                }
 #ifdef SWEEP_ABL_NOYTR
                 if (false) {
 #else
@@ -1333,19 +1441,37 @@ __global__ void __launch_bounds__(256, (P == 1 ? 2 : (K == 1 ? SWEEP_K1_MINB : 1
 #pragma unroll
                         for (int t = 0; t < NT; ++t) yt[k * NT + t] = ty[k][t];
                     if constexpr (RC > KT) yt[RC - 1] = 0.0;
+                    if constexpr (LL) {
 #pragma unroll
-                    for (int pi = 0; pi < KT2; ++pi)
-                        st_pair(ydst + (((size_t)ip * KT2 + pi) * NL + tid) * 2, yt[2 * pi], yt[2 * pi + 1]);
+                        for (int t = 0; t < KT; ++t) ll_store(ydst + (((size_t)ip * KT + t) * NL + tid) * 2, yt[t], tag_out);
+                    } else {
+#pragma unroll
+                        for (int pi = 0; pi < KT2; ++pi)
+                            st_pair(ydst + (((size_t)ip * KT2 + pi) * NL + tid) * 2, yt[2 * pi], yt[2 * pi + 1]);
+                    }
 #ifdef SWEEP_DEBUG
-                    SWEEP_DCHECK(ydst + ((size_t)ip + 1) * RC * NL <= prm.ytr + prm.ring_len);
+                    SWEEP_DCHECK(ydst + ((size_t)ip + 1) * RL * NL <= prm.ytr + prm.ring_len);
                     if (tid == 0) __stcg(prm.ytag + ((size_t)s * 2 + (J & 1)) * nxp + ip, J);
 #endif
+                }
+                // LL: the next column's lines, fetched after this column's solves (by then the strip
+                // below has usually written them: no round trip at the next column's start)
+                // (K > 2: not across a chunk boundary, where 4 K NT registers would live through
+                // phases C and A)
+                if (LL && J > 0 && ip + 1 < nxp && (K <= 2 || col + 1 < C)) ll_fetch(ip + 1);
+                if constexpr (BATCH) {
+                    // element r of this column: values [r NQ, (r+1) NQ) of usc
+                    auto sink = [&](int idx, double val) {
+                        const int r = idx / NQ;
+                        Sc[(size_t)(col * T + r) * SEL + dl * NQ + (idx - r * NQ)] = val;
+                    };
+                    ReduceScatter<T * NQ, LG / 2>::run(usc, lane, 0, T * NQ, sink);
                 }
             }
             // this buffer is refilled by the async proxy two chunks from now
             fence_proxy_async();
             __syncthreads();
-            if (tid == 0) {
+            if (!LL && tid == 0) {
                 // bar.sync orders every thread's trace-ring stores before thread 0's
                 // gpu-scope release (cumulative: the fence.acq_rel + relaxed store pattern
                 // of CUTLASS's inter-CTA barrier); a fence.sc before it (__threadfence)

@@ -105,6 +105,7 @@ struct sweep_handle {
     int n_dir_in, n_dir_eff;
     // schedule
     int log2gb, gb, kpl, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
+    int strip_a = 0, row_hi = 0, row_lo = 0;  // 2-D strip heights (balanced waves)
     size_t smem;
     int n_sm = 0;                 // SMs of the handle's device (queried at setup)
     bool scan1d = false;          // 1-D: warp-scan kernel (k_1d.cu); the fixup keeps the sequential kernel
@@ -577,13 +578,39 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             else h->err = "sweep2d kernel cannot be resident (registers/shared memory)";
             return bail(SWEEP_E_CUDA);
         }
+        // balanced strips: with P resident CTAs per stream, a whole number of waves of P strips,
+        // heights row_lo or row_lo + 1 <= T (a partial last wave idles CTAs at the end); not for
+        // the anti-diagonal (one group per lane) kernel, which runs every strip at T rows
+        h->strip_a = h->n_strips;
+        h->row_hi = h->row_lo = T;
+        const bool skew = h->kpl == 1 && h->gb == 1 && !(h->opt & sweepk::OPT_FIXUP);
+#ifndef SWEEP_BALANCE
+#define SWEEP_BALANCE 1
+#endif
+        if (SWEEP_BALANCE && !skew && T >= 2) {
+            const int P = std::max(1, bps * h->n_sm / h->n_streams);
+            const int nb = ((h->n_strips + P - 1) / P) * P;
+            const int lo = h->ny / nb;
+            if (nb > h->n_strips && lo >= 1 && lo < T) {
+                h->n_strips = nb;
+                h->row_lo = lo;
+                h->row_hi = lo + 1;
+                h->strip_a = h->ny - nb * lo;
+                h->n_tasks = h->n_strips * h->n_streams;
+            }
+        }
         h->grid = std::min(h->n_tasks, bps * h->n_sm);
         const int NT = h->np1;
         h->progress_ints = (size_t)h->n_streams * h->n_strips;
-        const int RC = 2 * ((h->kpl * NT + 1) / 2);  // ring record per lane: K*NT reals as pairs
-        h->ring_len = (size_t)h->n_streams * 2 * (h->n_chunks * C) * RC * h->block;
+        (void)NT;
+        // ring record per lane and column: K*NT reals as pairs, or as tagged LL lines
+        const int RL = sweepk::sweep2d_ring_record(h->p, h->kpl, h->log2gb, h->opt);
+        h->ring_len = (size_t)h->n_streams * 2 * (h->n_chunks * C) * RL * h->block;
         if ((ce = cudaMalloc(&h->d_ytr, sizeof(double) * h->ring_len)))
             return cuda_fail(h, ce, "cudaMalloc ytr"), bail(SWEEP_E_CUDA);
+        // LL lines carry the tag of the run that wrote them: no stale memory may match a tag
+        if ((ce = cudaMemset(h->d_ytr, 0, sizeof(double) * h->ring_len)))
+            return cuda_fail(h, ce, "memset ytr"), bail(SWEEP_E_CUDA);
         if (sweepk::debug_build()) {
             const size_t ntag = (size_t)h->n_streams * 2 * (h->n_chunks * C);
             if ((ce = cudaMalloc(&h->d_ytag, sizeof(int) * ntag)))
@@ -663,11 +690,12 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
     if ((ce = cudaMemcpy(h->d_streams, streams.data(), sizeof(StreamDesc) * streams.size(), cudaMemcpyHostToDevice)))
         return cuda_fail(h, ce, "copy streams"), bail(SWEEP_E_CUDA);
     // progress flags | task counter | error flag, contiguous so one memset resets them
-    if ((ce = cudaMalloc(&h->d_progress, sizeof(int) * (h->progress_ints + 2))))
+    // progress flags | task counter | error flag | launch epoch (LL ring tags)
+    if ((ce = cudaMalloc(&h->d_progress, sizeof(int) * (h->progress_ints + 3))))
         return cuda_fail(h, ce, "cudaMalloc flags"), bail(SWEEP_E_CUDA);
     h->d_counter = h->d_progress + h->progress_ints;
     h->d_err = h->d_counter + 1;
-    if ((ce = cudaMemset(h->d_progress, 0, sizeof(int) * (h->progress_ints + 2))))
+    if ((ce = cudaMemset(h->d_progress, 0, sizeof(int) * (h->progress_ints + 3))))
         return cuda_fail(h, ce, "memset flags"), bail(SWEEP_E_CUDA);
     if ((ce = cudaMalloc(&h->d_slabs, sizeof(double) * h->out_size * (size_t)h->n_streams)))
         return cuda_fail(h, ce, "cudaMalloc slabs"), bail(SWEEP_E_CUDA);
@@ -742,6 +770,9 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
                           : 0;
         prm.n_streams = h->n_streams;
         prm.n_strips = h->n_strips;
+        prm.strip_a = h->strip_a;
+        prm.row_hi = h->row_hi;
+        prm.row_lo = h->row_lo;
         prm.n_chunks = h->n_chunks;
         prm.n_tasks = h->n_tasks;
         prm.gb = h->gb;
@@ -757,6 +788,7 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.dirs = h->d_dirs;
         prm.streams = h->d_streams;
         prm.progress = h->d_progress;
+        prm.epoch = h->d_err + 1;
         prm.task_counter = h->d_counter;
         prm.ytr = h->d_ytr;
         prm.ring_len = h->ring_len;

@@ -51,6 +51,7 @@ struct Sweep2DParams {
     int nx, ny, G;                 // G = groups on this rank
     int nx_pad;                    // n_chunks * C (trace ring row length)
     int n_streams, n_strips, n_chunks, n_tasks;
+    int strip_a, row_hi, row_lo;   // strips 0..strip_a-1 have row_hi rows, later ones row_lo (<= T)
     int gb;                        // lanes per direction (power of 2)
     int kpl;                       // groups per lane
     int dset;                      // directions per CTA
@@ -64,7 +65,9 @@ struct Sweep2DParams {
     const double* inflow;          // [N_bnode][G]
     const DirConst* dirs;          // quadrant-sorted
     const StreamDesc* streams;
-    int* progress;                 // [n_streams][n_strips] chunks completed
+    int* progress;                 // [n_streams][n_strips] chunks completed (per-chunk flag protocol)
+    int* epoch;                    // LL ring protocol: launches completed on this handle (device counter,
+                                   // read at kernel start, bumped by the last CTA: graph replays too)
     int* task_counter;
     double* ytr;                   // [n_streams][2][nx][K][NT][NL]
     size_t ring_len;               // doubles in ytr
@@ -134,6 +137,7 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt);
 int sweep2d_occupancy(int p, int log2lg, int k, int opt, int block, size_t smem, int* blocks_per_sm);
 int sweep2d_rows_per_strip(int p, int k);
 int sweep2d_cols_per_chunk(int p, int k, int opt);
+int sweep2d_ring_record(int p, int k, int log2lg, int opt);  // trace-ring doubles per lane and column
 const char* cuda_err_string(int e);
 int fp64_probe(int device, double* tflops);
 int launch_floor(int device, int reps, double* us);

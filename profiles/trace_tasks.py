@@ -15,8 +15,9 @@ import synth  # noqa: E402
 import torch  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
-so = "/tmp/libsweep_trace.so"
-B.build(extra=["-DSWEEP_TRACE"], out=so)
+so = os.environ.get("TRACE_SO") or "/tmp/libsweep_trace.so"
+if not os.environ.get("TRACE_SO"):
+    B.build(extra=["-DSWEEP_TRACE"], out=so)
 S._lib = None
 lib = S.load_library(so)
 prob = synth.config(cfg)

@@ -31,9 +31,10 @@ def test_roofline_model():
     sys.path.insert(0, ROOT)
     import bench
     import synth
-    # C5: 144.4 flops per (element, distinct direction, group) with 16 directions per quadrant
+    # C5: 132.4 flops per (element, distinct direction, group) with 16 directions per quadrant
+    # (144.4 before the round-2 half-sum / half-difference lifts: 40 instead of 52 lift flops)
     f = bench.flops_per_edg(2, 2, 16, 32)
-    assert 140 < f < 150
+    assert 130 < f < 135
     prob = synth.config(1)
     assert bench.algorithmic_bytes(prob) == 8 * (prob.sigma.size + prob.q.size + prob.inflow.size +
                                                  prob.n_el * prob.n * 3 + 2 * prob.n_bnode)

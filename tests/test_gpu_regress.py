@@ -170,3 +170,46 @@ def test_structured_solves_match_dense_lu(pk, p):
     for seed in (1, 2):
         err = pk.selfcheck_solves(p, 1 << 20, seed)
         assert 0.0 <= err <= 1e-12, (p, seed, err)
+
+
+@pytest.mark.parametrize("cfg,nx,G", [(4, 96, 32), (5, 160, 8), (5, 96, 16), (4, 40, 3)])
+def test_ll_ring_repeat_graph_host(pk, cfg, nx, G):
+    """The LL strip hand-off (tagged trace lines) on the one- and two-groups-per-
+    lane kernels: repeated runs of one handle, CUDA-graph replays (the kernel's tags come from
+    a device-side launch epoch, so a replay can never take a line of the previous replay for
+    its own, even after its inputs change) and host-API runs all give bitwise the same gray
+    output as a fresh handle, with no device error; and that output matches the oracle."""
+    import torch
+    prob = synth.config(cfg, nx=nx, G=G)
+    dev = torch.device("cuda:0")
+    sig, q, fl = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (prob.sigma, prob.q, prob.inflow))
+    sw = pk.from_problem(prob)
+    sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+    ref = sw.closures_get().cpu().clone()
+    assert_parity(ref.numpy(), oracle.sweep(prob), prob.dim, prob.nx, prob.ny, prob.p)
+    for _ in range(5):
+        sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+        assert torch.equal(sw.closures_get().cpu(), ref)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            sw.sweep_run(sig, prob.inv_c_dt, q, fl)
+    torch.cuda.synchronize()
+    for _ in range(5):
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(sw.closures_get().cpu(), ref)
+    q.mul_(1.5)   # new inputs under the same graph
+    fresh = pk.from_problem(prob)
+    fresh.sweep_run(sig, prob.inv_c_dt, q, fl)
+    ref2 = fresh.closures_get().cpu().clone()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(sw.closures_get().cpu(), ref2)
+    hs, hq, hf = (x.cpu().numpy() for x in (sig, q, fl))
+    out = sw.sweep_run_host(hs, prob.inv_c_dt, np.ascontiguousarray(hq), hf)
+    assert np.array_equal(out, ref2.numpy())
