@@ -38,7 +38,7 @@
 
 // ablation switches give wrong results by design (timing experiments only)
 #if (defined(SWEEP_ABL_NOPHASEC) || defined(SWEEP_ABL_NOWAIT) || defined(SWEEP_ABL_NOYTR) || \
-     defined(SWEEP_ABL_NORED)) && !defined(SWEEP_EXPERIMENTS)
+     defined(SWEEP_ABL_NORED) || defined(SWEEP_ABL_RELAXED)) && !defined(SWEEP_EXPERIMENTS)
 #error "SWEEP_ABL_* switches are for experiment builds only (scripts/build_variants.py)"
 #endif
 
@@ -689,9 +689,8 @@ __global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P =
             cx = prm.dirs[sd.d0 + dl].cx;
             cy = prm.dirs[sd.d0 + dl].cy;
         }
-        // balanced strips (host): strip_a strips of row_hi rows, then strips of row_lo rows
-        const int j0 = (J < prm.strip_a) ? J * prm.row_hi : prm.strip_a * prm.row_hi + (J - prm.strip_a) * prm.row_lo;
-        const int rows = min((J < prm.strip_a) ? prm.row_hi : prm.row_lo, ny - j0);
+        const int j0 = J * T;
+        const int rows = min(T, ny - j0);
         double* slab = prm.slabs + (size_t)s * prm.out_size;
         const bool bulk = prm.bulk_ok && ((sd.ng & 1) == 0) && ((sd.g0 & 1) == 0);
 
@@ -1366,15 +1365,6 @@ __global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P =
 #pragma unroll
                 for (int r = 0; r < T; ++r) {
                     const int el = col * T + r;
-                    if (r >= rows) {
-                        // a short strip (balanced heights): no element; the y-trace passes on
-                        // from the strip's top row
-                        if constexpr (BATCH) {
-#pragma unroll
-                            for (int m = 0; m < NQ; ++m) usc[r * NQ + m] = 0.0;
-                        }
-                        continue;
-                    }
                     // us: group sum of the modal solution; SIG also the sigma-weighted sum
                     double us[SIG ? 2 * NQ : NQ];
 #pragma unroll
@@ -1476,7 +1466,12 @@ __global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P =
                 // gpu-scope release (cumulative: the fence.acq_rel + relaxed store pattern
                 // of CUTLASS's inter-CTA barrier); a fence.sc before it (__threadfence)
                 // only added latency to every hop of the strip chain (C4 1.07 -> 1.02 ms)
+#ifdef SWEEP_ABL_RELAXED
+                // timing ablation: no release fence (the ring stores may arrive after the flag)
+                asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(prm.progress + (size_t)s * prm.n_strips + J), "r"(c + 1) : "memory");
+#else
                 st_release(prm.progress + (size_t)s * prm.n_strips + J, c + 1);
+#endif
             }
 #ifdef SWEEP_TRACE
             long long tc2 = clock64();

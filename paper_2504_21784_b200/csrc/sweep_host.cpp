@@ -105,7 +105,6 @@ struct sweep_handle {
     int n_dir_in, n_dir_eff;
     // schedule
     int log2gb, gb, kpl, block, dset, n_streams, n_strips, n_chunks, n_tasks, grid, nseg, seglen;
-    int strip_a = 0, row_hi = 0, row_lo = 0;  // 2-D strip heights (balanced waves)
     size_t smem;
     int n_sm = 0;                 // SMs of the handle's device (queried at setup)
     bool scan1d = false;          // 1-D: warp-scan kernel (k_1d.cu); the fixup keeps the sequential kernel
@@ -578,27 +577,6 @@ extern "C" int sweep_setup(const sweep_desc* desc, sweep_handle** out) {
             else h->err = "sweep2d kernel cannot be resident (registers/shared memory)";
             return bail(SWEEP_E_CUDA);
         }
-        // balanced strips: with P resident CTAs per stream, a whole number of waves of P strips,
-        // heights row_lo or row_lo + 1 <= T (a partial last wave idles CTAs at the end); not for
-        // the anti-diagonal (one group per lane) kernel, which runs every strip at T rows
-        h->strip_a = h->n_strips;
-        h->row_hi = h->row_lo = T;
-        const bool skew = h->kpl == 1 && h->gb == 1 && !(h->opt & sweepk::OPT_FIXUP);
-#ifndef SWEEP_BALANCE
-#define SWEEP_BALANCE 1
-#endif
-        if (SWEEP_BALANCE && !skew && T >= 2) {
-            const int P = std::max(1, bps * h->n_sm / h->n_streams);
-            const int nb = ((h->n_strips + P - 1) / P) * P;
-            const int lo = h->ny / nb;
-            if (nb > h->n_strips && lo >= 1 && lo < T) {
-                h->n_strips = nb;
-                h->row_lo = lo;
-                h->row_hi = lo + 1;
-                h->strip_a = h->ny - nb * lo;
-                h->n_tasks = h->n_strips * h->n_streams;
-            }
-        }
         h->grid = std::min(h->n_tasks, bps * h->n_sm);
         const int NT = h->np1;
         h->progress_ints = (size_t)h->n_streams * h->n_strips;
@@ -770,9 +748,6 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
                           : 0;
         prm.n_streams = h->n_streams;
         prm.n_strips = h->n_strips;
-        prm.strip_a = h->strip_a;
-        prm.row_hi = h->row_hi;
-        prm.row_lo = h->row_lo;
         prm.n_chunks = h->n_chunks;
         prm.n_tasks = h->n_tasks;
         prm.gb = h->gb;

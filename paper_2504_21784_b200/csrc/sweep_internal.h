@@ -51,7 +51,6 @@ struct Sweep2DParams {
     int nx, ny, G;                 // G = groups on this rank
     int nx_pad;                    // n_chunks * C (trace ring row length)
     int n_streams, n_strips, n_chunks, n_tasks;
-    int strip_a, row_hi, row_lo;   // strips 0..strip_a-1 have row_hi rows, later ones row_lo (<= T)
     int gb;                        // lanes per direction (power of 2)
     int kpl;                       // groups per lane
     int dset;                      // directions per CTA

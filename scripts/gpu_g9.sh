@@ -1,6 +1,6 @@
 B="--no-e2e --no-cpu --no-floors --no-parity --steps 10"
 for rep in 1 2; do
-for v in prod nobal; do
+for v in prod nobal nobalng; do
   L=""; [ "$v" != prod ] && L="--lib build/$v.so"
   for a in "--config 5" "--config 4" "--rank-of 8" "--rank-of 4"; do
     t=$(echo $a | tr -d ' -')
