@@ -230,7 +230,9 @@ int sweep2d_smem_bytes(int p, int k, int gbk, int dset, int opt) {
     const bool defer = SWEEP_DEFER_C && !(k == 1 && gbk == 1);
     const int s2 = ((opt & OPT_SIGMA) || defer) ? CT * (dset * NQ + 1) : 0;
     const int rc = 2 * ((k * (p + 1) + 1) / 2);  // trace-ring record per lane (pairs of doubles)
-    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + ((dset * 16 + 1) & ~1) + rc * NL + 81 + s2) *
+    // group-sum scratch of the shared-memory reduction (+ 2 doubles of 16-byte alignment)
+    const int red = smem_red(p, k, gbk / k, opt) ? (NL / 32) * CT / C * NQ * kRedRow + 2 : 0;
+    return (2 * (CT * NN * gbk + CT * gbk) + CT * (dset * NQ + 1) + ((dset * 16 + 1) & ~1) + rc * NL + 81 + s2 + red) *
            (int)sizeof(double);
 }
 int sweep2d_rows_per_strip(int p, int k) { return rows_per_strip(p, k); }

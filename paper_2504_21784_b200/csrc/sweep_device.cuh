@@ -186,6 +186,48 @@ struct ReduceScatter {
     }
 };
 
+// Sum over the LG lanes of each direction of a warp (D = 32 / LG directions) of V values per
+// lane, through the warp's scratch rows scr[V][kRedRow]: every lane stores its V values, then
+// output (d, v) is summed in lane order l = 0..LG-1 (fixed: bitwise repeatable) by SPL lanes
+// of LG / SPL values each, combined with shuffles; sink(d, v, sum) runs on one lane per output.
+constexpr int kRedRow = 34;  // scratch row: 32 lane values + 2 doubles of padding
+template <int V, int LG, class Sink>
+__device__ __forceinline__ void group_sum_smem(const double (&v)[V], double* scr, int lane, Sink& sink) {
+    constexpr int D = 32 / LG, NO = D * V;
+    // lanes per output: a power of two <= min(32 / NO, LG / 2)
+    constexpr int SPLM = (NO >= 32) ? 1 : (32 / NO >= LG / 2 ? LG / 2 : 32 / NO);
+    constexpr int SPL = SPLM >= 16 ? 16 : SPLM >= 8 ? 8 : SPLM >= 4 ? 4 : SPLM >= 2 ? 2 : 1;
+    constexpr int PER = LG / SPL;                                                 // values per lane
+    static_assert(PER % 2 == 0, "16-byte reads");
+#pragma unroll
+    for (int k = 0; k < V; ++k) scr[k * kRedRow + lane] = v[k];
+    __syncwarp();
+    constexpr int STEP = 32 / SPL;  // outputs per pass
+    for (int o0 = 0; o0 < NO; o0 += STEP) {
+        const int o = o0 + lane % STEP, part = lane / STEP;
+        double acc = 0.0;
+        int d = 0, k = 0;
+        if (o < NO) {
+            d = o / V;
+            k = o - d * V;
+            const double2* p = reinterpret_cast<const double2*>(scr + k * kRedRow + d * LG + part * PER);
+#pragma unroll
+            for (int i = 0; i < PER / 2; ++i) {
+                const double2 t = p[i];
+                acc = (i == 0) ? t.x + t.y : (acc + t.x) + t.y;
+            }
+        }
+#pragma unroll
+        for (int m = STEP; m < 32; m <<= 1) {
+            // partial sums of one output sit STEP lanes apart; the lower part keeps the order
+            const double other = __shfl_down_sync(FULLMASK, acc, m);
+            if ((lane / STEP) % (2 * (m / STEP)) == 0) acc = acc + other;
+        }
+        if (part == 0 && o < NO) sink(d, k, acc);
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------------ 2-D, p = 2
 struct LaneP2 {
     double lx0, lx1r, lx1i, ly0, ly1r, ly1i;   // lifts 6 cx W[.][0], 6 cy W[.][0]
@@ -474,6 +516,20 @@ __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
 #endif
 __host__ __device__ constexpr bool ll_ring(int P, int K, int LG, int OPT) {
     return SWEEP_LL && K <= SWEEP_LL_KMAX && !(K == 1 && LG == 1 && !(OPT & OPT_FIXUP)) && P >= 1;
+}
+// Group sums of a column through a per-warp shared-memory transpose instead of the shuffle
+// reduce-scatter, for the p = 2 one-group-per-lane layout with a group reduction (the 8-group
+// rank of a group-sharded C5): the reduce-scatter costs ~9 instructions per value and stage
+// (2 shuffles, 4 selects, moves, an add), and with one solve chain per lane the warps are
+// issue-bound.  Measured (same box): 8-group rank 3.13 -> 2.87 ms; C4 (p = 1) 0.600 -> 0.607,
+// the K = 2 ranks 4.03 -> 6.20 / 6.96 -> 7.47 ms (spills) -- so only there.  Rows of 32 lane
+// values, padded to 34 doubles (16-byte aligned rows, conflict-free 16-byte reads down a
+// column of rows).
+#ifndef SWEEP_SMEMRED
+#define SWEEP_SMEMRED 1
+#endif
+__host__ __device__ constexpr bool smem_red(int P, int K, int LG, int OPT) {
+    return SWEEP_SMEMRED && P == 2 && K == 1 && LG > 1 && !(OPT & (OPT_SIGMA | OPT_FIXUP));
 }
 // doubles per lane and column in the trace ring
 __host__ __device__ constexpr int ring_record(int P, int K, int LG, int OPT) {
@@ -772,6 +828,11 @@ __global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P =
         // limit) and not for one group per direction (C3: 0.324 -> 0.347 ms)
         constexpr bool DEFER = SWEEP_DEFER_C && !SIG && !(K == 1 && LG == 1);
         double* Salt = S2 + (SIG ? (size_t)CT * SEL : 0);  // DEFER: S of the odd chunks
+        // SMEMRED: per-warp group-sum scratch [T NQ][kRedRow] (16-byte aligned)
+        constexpr bool SMEMRED = smem_red(P, K, LG, OPT);
+        double* redS = reinterpret_cast<double*>(
+            (reinterpret_cast<uintptr_t>(Salt + (DEFER ? (size_t)CT * SEL : 0)) + 15) & ~uintptr_t(15));
+        double* redW = redS + (size_t)(tid >> 5) * (T * NQ * kRedRow);
         const size_t sig_off = 6 * nodes + 2 * (size_t)prm.nbnode;  // SIG: sigma phi | sigma J
         // (compile-time constant-bank indices only: ptxas hoists constant loads out of
         // the task loop for every thread, and a thread-dependent index past the end of
@@ -1449,7 +1510,14 @@ __global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P =
                 // (K > 2: not across a chunk boundary, where 4 K NT registers would live through
                 // phases C and A)
                 if (LL && J > 0 && ip + 1 < nxp && (K <= 2 || col + 1 < C)) ll_fetch(ip + 1);
-                if constexpr (BATCH) {
+                if constexpr (BATCH && SMEMRED) {
+                    // output (direction d of this warp, value v = r NQ + m)
+                    auto sink = [&](int d, int v, double val) {
+                        const int r = v / NQ;
+                        Sc[(size_t)(col * T + r) * SEL + ((tid >> 5) * (32 / LG) + d) * NQ + (v - r * NQ)] = val;
+                    };
+                    group_sum_smem<T * NQ, LG>(usc, redW, lane, sink);
+                } else if constexpr (BATCH) {
                     // element r of this column: values [r NQ, (r+1) NQ) of usc
                     auto sink = [&](int idx, double val) {
                         const int r = idx / NQ;
