@@ -490,8 +490,11 @@ __device__ __forceinline__ void solve_p1(const LaneP1& L, double st, const doubl
 #ifndef SWEEP_ROWS_K4
 #define SWEEP_ROWS_K4 2
 #endif
+#ifndef SWEEP_ROWS_K2
+#define SWEEP_ROWS_K2 4
+#endif
 __host__ __device__ constexpr int rows_per_strip(int P, int K) {
-    return K >= 4 ? SWEEP_ROWS_K4 : (K == 2 ? 4 : (P == 2 ? SWEEP_ROWS_P2K1 : SWEEP_ROWS_P1K1));
+    return K >= 4 ? SWEEP_ROWS_K4 : (K == 2 ? SWEEP_ROWS_K2 : (P == 2 ? SWEEP_ROWS_P2K1 : SWEEP_ROWS_P1K1));
 }
 #ifndef SWEEP_COLS_K4
 #define SWEEP_COLS_K4 8
@@ -499,8 +502,15 @@ __host__ __device__ constexpr int rows_per_strip(int P, int K) {
 #ifndef SWEEP_COLS_K4_SIG
 #define SWEEP_COLS_K4_SIG 8  // with the second S buffer the chunk still fits (228 KB): C5 sigma 14.26 -> 13.97 ms vs 4
 #endif
+#ifndef SWEEP_COLS_K2
+#define SWEEP_COLS_K2 SWEEP_COLS_K1
+#endif
+#ifndef SWEEP_COLS_P2K1
+#define SWEEP_COLS_P2K1 SWEEP_COLS_K1
+#endif
 __host__ __device__ constexpr int cols_per_chunk(int P, int K, int OPT = 0) {
-    return K >= 4 ? ((OPT & OPT_SIGMA) ? SWEEP_COLS_K4_SIG : SWEEP_COLS_K4) : SWEEP_COLS_K1;  // sigma moments: a second S buffer
+    return K >= 4 ? ((OPT & OPT_SIGMA) ? SWEEP_COLS_K4_SIG : SWEEP_COLS_K4)  // sigma moments: a second S buffer
+                  : (K == 2 ? SWEEP_COLS_K2 : (P == 2 ? SWEEP_COLS_P2K1 : SWEEP_COLS_K1));
 }
 // (K = 2: T = 4 rows, C = 4 columns -> 16 elements per chunk, like K = 4)
 __host__ __device__ constexpr int nq_of(int P) { return P == 2 ? 9 : 4; }
