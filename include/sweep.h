@@ -131,7 +131,10 @@ int sweep_layout(const sweep_handle *h, size_t off[8], size_t *total_doubles);
  *   d_q      [N_el][n][G_loc]    nodal isotropic source q_g (reading R2: no 1/(4 pi))
  *   d_inflow [N_bnode][G_loc]    isotropic inflow per boundary face node (0 = vacuum)
  * inv_c_dt = 1/(c dt) > 0 is added to sigma_t.  Group is the
- * fastest index.  Ends with the in-place NCCL all-reduce when nranks > 1. */
+ * fastest index.  Ends with the in-place NCCL all-reduce when nranks > 1.
+ * May be captured into a CUDA graph and replayed (also with new contents of the
+ * input buffers): the strip hand-off tags come from a device-side launch counter,
+ * not from the host.  Runs of one handle must be stream-ordered (not concurrent). */
 int sweep_run(sweep_handle *h, const double *d_sigma, double inv_c_dt, const double *d_q,
               const double *d_inflow, void *cuda_stream);
 
