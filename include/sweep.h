@@ -145,7 +145,13 @@ int closures_get(sweep_handle *h, double *out, size_t n_doubles, void *cuda_stre
 
 /* End-to-end convenience call with HOST buffers (pinned recommended): copies
  * the inputs host->device into library-owned buffers, runs the sweep, copies
- * the packed output device->host and synchronises.  Same shapes as sweep_run. */
+ * the packed output device->host and synchronises.  Same shapes as sweep_run.
+ * 2-D: the copy overlaps the sweep -- bands of 8 mesh rows are copied on a
+ * library-owned stream from both ends of the mesh inwards, each followed by a
+ * stream write of the band's ready flag (cuStreamWriteValue32), and every strip
+ * of the sweep kernel waits for the flags of its rows (pinned buffers give the
+ * overlap; pageable ones are copied before the launch).  Calls on one handle
+ * must be stream-ordered (the staging buffers are reused). */
 int sweep_run_host(sweep_handle *h, const double *h_sigma, double inv_c_dt, const double *h_q,
                    const double *h_inflow, double *h_out, size_t n_doubles, void *cuda_stream);
 

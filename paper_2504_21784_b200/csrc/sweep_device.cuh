@@ -110,6 +110,12 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// system-scope acquire: flags written by a stream memory operation (sweep_run_host's copy stream)
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -819,6 +825,24 @@ __global__ void __launch_bounds__((P == 2 && K == 1) ? SWEEP_K1_MAXT : 256, (P =
                 cp_async_wait<0>();
             }
         };
+        // sweep_run_host: this strip's physical rows (and the inflow, copied before every band)
+        // arrive by a host->device copy that overlaps the sweep; the copy stream writes band b's
+        // flag (preceded by a system-scope fence) once its q and sigma rows have landed
+        if (prm.in_ready) {
+            if (tid == 0) {
+                const int jl = fy ? ny - j0 - rows : j0;  // lowest physical row of the strip
+                const long long t_start = clock64();
+                for (int b = jl / prm.in_band_rows; b <= (jl + rows - 1) / prm.in_band_rows; ++b)
+                    while (ld_acquire_sys(prm.in_ready + b) - prm.in_gen < 0) {
+                        if (clock64() - t_start > (1LL << 36) || (ld_relaxed_gpu(prm.err) & 4)) {
+                            atomicOr(prm.err, 4);
+                            break;
+                        }
+                    }
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk copies read them next
+            }
+            __syncthreads();
+        }
         stage(0, 0);
         // phase-C weights of this stream's directions: [dd][14]
         double* coefS = S + (size_t)CT * SEL;

@@ -124,8 +124,13 @@ struct sweep_handle {
     int* d_err = nullptr;
     int* d_counter = nullptr;
     size_t progress_ints = 0;
-    // host-API staging
+    // host-API staging; 2-D: the copy stream, its order / join events and the per-band
+    // input-ready flags of the overlapped copy (sweep_run_host)
     double *d_in_sigma = nullptr, *d_in_q = nullptr, *d_in_inflow = nullptr;
+    cudaStream_t cp_stream = nullptr;
+    cudaEvent_t cp_ev[2] = {nullptr, nullptr};
+    int* d_in_ready = nullptr;
+    int in_gen = 0;
     // unaccelerated TRT iteration workspace (trt_step)
     double *d_trt_q = nullptr, *d_trt_nu = nullptr, *d_trt_part = nullptr, *d_trt_norm = nullptr;
     double* d_trt_E = nullptr;  // E^l of the outer iteration (eq:relative_tol, u = [T, E])
@@ -708,8 +713,23 @@ extern "C" int sweep_layout(const sweep_handle* h, size_t off[8], size_t* total)
     return SWEEP_OK;
 }
 
+// InputBands: the 2-D kernel's per-band input-ready flags (sweep_run_host's overlapped copy);
+// ready == nullptr: the inputs are resident when the kernel starts
+struct InputBands {
+    const int* ready = nullptr;
+    int gen = 0, band_rows = 1;
+};
+
+static int run_impl(sweep_handle* h, const double* d_sigma, double inv_c_dt, const double* d_q,
+                    const double* d_inflow, void* stream, InputBands bands);
+
 extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt, const double* d_q,
                          const double* d_inflow, void* stream) {
+    return run_impl(h, d_sigma, inv_c_dt, d_q, d_inflow, stream, InputBands{});
+}
+
+static int run_impl(sweep_handle* h, const double* d_sigma, double inv_c_dt, const double* d_q,
+                    const double* d_inflow, void* stream, InputBands bands) {
     NvtxRange nv("sweep_run");
     if (!h) return SWEEP_E_ARG;
     if (!d_sigma || !d_q || !d_inflow) return fail(h, SWEEP_E_ARG, "null input pointer");
@@ -772,6 +792,9 @@ extern "C" int sweep_run(sweep_handle* h, const double* d_sigma, double inv_c_dt
         prm.out_size = h->out_size;
         prm.nodes = h->nodes;
         prm.err = h->d_err;
+        prm.in_ready = bands.ready;
+        prm.in_gen = bands.gen;
+        prm.in_band_rows = bands.band_rows;
         e = sweepk::launch_sweep2d(h->p, h->log2gb, h->kpl, h->opt, prm, h->grid, h->block, h->smem, stream);
     } else if (h->scan1d) {
         sweepk::Sweep1DScanParams prm;
@@ -933,6 +956,23 @@ extern "C" int closures_get(sweep_handle* h, double* out, size_t n, void* stream
     return SWEEP_OK;
 }
 
+// cuStreamWriteValue32 from the driver the runtime loaded (no link-time libcuda dependency);
+// nullptr if unavailable (sweep_run_host then copies before the sweep)
+using WriteValue32Fn = int (*)(void* stream, unsigned long long addr, unsigned value, unsigned flags);
+static WriteValue32Fn write_value32() {
+    static WriteValue32Fn fn = []() -> WriteValue32Fn {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return reinterpret_cast<WriteValue32Fn>(f);
+    }();
+    return fn;
+}
+
 extern "C" int sweep_run_host(sweep_handle* h, const double* h_sigma, double inv_c_dt, const double* h_q,
                               const double* h_inflow, double* h_out, size_t n, void* stream) {
     if (!h || !h_sigma || !h_q || !h_inflow || !h_out) return SWEEP_E_ARG;
@@ -945,6 +985,53 @@ extern "C" int sweep_run_host(sweep_handle* h, const double* h_sigma, double inv
         if ((ce = cudaMalloc(&h->d_in_inflow, sizeof(double) * nf))) return cuda_fail(h, ce, "cudaMalloc staging");
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (h->dim == 2 && write_value32()) {
+        // 2-D: the copy overlaps the sweep.  Bands of kBandRows physical rows are copied on a
+        // copy stream from both ends of the mesh inwards (the order in which the +y and -y
+        // quadrant streams reach them); after each band a stream memory operation (no SM
+        // needed, preceded by a system-scope fence) writes the band's flag = this run's
+        // generation, and every strip of the kernel waits for the flags of its rows.
+        constexpr int kBandRows = 8;
+        const int nb = (h->ny + kBandRows - 1) / kBandRows;
+        if (!h->cp_stream) {
+            if ((ce = cudaStreamCreateWithFlags(&h->cp_stream, cudaStreamNonBlocking))) return cuda_fail(h, ce, "copy stream");
+            if ((ce = cudaEventCreateWithFlags(&h->cp_ev[0], cudaEventDisableTiming))) return cuda_fail(h, ce, "copy event");
+            if ((ce = cudaEventCreateWithFlags(&h->cp_ev[1], cudaEventDisableTiming))) return cuda_fail(h, ce, "copy event");
+            if ((ce = cudaMalloc(&h->d_in_ready, sizeof(int) * nb))) return cuda_fail(h, ce, "cudaMalloc band flags");
+            if ((ce = cudaMemset(h->d_in_ready, 0, sizeof(int) * nb))) return cuda_fail(h, ce, "memset band flags");
+        }
+        if (++h->in_gen <= 0) {  // generation wrap (2^31 runs): restart from 1 with cleared flags
+            h->in_gen = 1;
+            if ((ce = cudaMemsetAsync(h->d_in_ready, 0, sizeof(int) * nb, st))) return cuda_fail(h, ce, "memset band flags");
+        }
+        cudaStream_t cp = h->cp_stream;
+        // the staging buffers are free once the work queued on st so far is done
+        if ((ce = cudaEventRecord(h->cp_ev[0], st)) || (ce = cudaStreamWaitEvent(cp, h->cp_ev[0], 0)))
+            return cuda_fail(h, ce, "copy stream order");
+        if ((ce = cudaMemcpyAsync(h->d_in_inflow, h_inflow, sizeof(double) * nf, cudaMemcpyHostToDevice, cp))) return cuda_fail(h, ce, "H2D");
+        const size_t row_s = (size_t)h->nx * h->G, row_q = row_s * h->n;
+        for (int k = 0; k < nb; ++k) {
+            const int b = (k & 1) ? nb - 1 - k / 2 : k / 2;
+            const size_t j0 = (size_t)b * kBandRows, nr = std::min<size_t>(kBandRows, h->ny - j0);
+            if ((ce = cudaMemcpyAsync(h->d_in_q + j0 * row_q, h_q + j0 * row_q, sizeof(double) * nr * row_q,
+                                      cudaMemcpyHostToDevice, cp)) ||
+                (ce = cudaMemcpyAsync(h->d_in_sigma + j0 * row_s, h_sigma + j0 * row_s, sizeof(double) * nr * row_s,
+                                      cudaMemcpyHostToDevice, cp)))
+                return cuda_fail(h, ce, "H2D");
+            const int rv = write_value32()(cp, reinterpret_cast<unsigned long long>(h->d_in_ready + b), (unsigned)h->in_gen, 0);
+            if (rv) return fail(h, SWEEP_E_CUDA, "cuStreamWriteValue32 failed: " + std::to_string(rv));
+        }
+        if ((ce = cudaEventRecord(h->cp_ev[1], cp))) return cuda_fail(h, ce, "copy event");
+        InputBands bands;
+        bands.ready = h->d_in_ready;
+        bands.gen = h->in_gen;
+        bands.band_rows = kBandRows;
+        int r = run_impl(h, h->d_in_sigma, inv_c_dt, h->d_in_q, h->d_in_inflow, stream, bands);
+        // join: later work on st (and the next run's copies) is ordered after the copies
+        if ((ce = cudaStreamWaitEvent(st, h->cp_ev[1], 0))) return cuda_fail(h, ce, "copy join");
+        if (r) return r;
+        return closures_get(h, h_out, n, stream);
+    }
     if ((ce = cudaMemcpyAsync(h->d_in_sigma, h_sigma, sizeof(double) * ns, cudaMemcpyHostToDevice, st))) return cuda_fail(h, ce, "H2D");
     if ((ce = cudaMemcpyAsync(h->d_in_q, h_q, sizeof(double) * nq, cudaMemcpyHostToDevice, st))) return cuda_fail(h, ce, "H2D");
     if ((ce = cudaMemcpyAsync(h->d_in_inflow, h_inflow, sizeof(double) * nf, cudaMemcpyHostToDevice, st))) return cuda_fail(h, ce, "H2D");
@@ -1083,6 +1170,13 @@ extern "C" void sweep_destroy(sweep_handle* h) {
     cudaFree(h->d_in_sigma);
     cudaFree(h->d_in_q);
     cudaFree(h->d_in_inflow);
+    cudaFree(h->d_in_ready);
+    if (h->cp_stream) {
+        cudaStreamSynchronize(h->cp_stream);
+        cudaStreamDestroy(h->cp_stream);
+    }
+    for (auto& e : h->cp_ev)
+        if (e) cudaEventDestroy(e);
     delete h;
 }
 

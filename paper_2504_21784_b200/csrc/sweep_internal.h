@@ -75,6 +75,8 @@ struct Sweep2DParams {
     size_t out_size;
     size_t nodes;                  // N_el * n
     int* err;
+    const int* in_ready;           // sweep_run_host: per band of in_band_rows physical rows, the generation
+    int in_gen, in_band_rows;      // whose inputs have landed (nullptr: inputs resident at launch)
 };
 
 struct Sweep1DParams {
