@@ -151,7 +151,8 @@ int closures_get(sweep_handle *h, double *out, size_t n_doubles, void *cuda_stre
  * stream write of the band's ready flag (cuStreamWriteValue32), and every strip
  * of the sweep kernel waits for the flags of its rows (pinned buffers give the
  * overlap; pageable ones are copied before the launch).  Calls on one handle
- * must be stream-ordered (the staging buffers are reused). */
+ * must be stream-ordered (the staging buffers are reused).  Not capturable into a
+ * CUDA graph (it synchronises cuda_stream; the flag generation is a host counter). */
 int sweep_run_host(sweep_handle *h, const double *h_sigma, double inv_c_dt, const double *h_q,
                    const double *h_inflow, double *h_out, size_t n_doubles, void *cuda_stream);
 
