@@ -1167,14 +1167,14 @@ extern "C" void sweep_destroy(sweep_handle* h) {
     cudaFree(h->d_ytag);
     cudaFree(h->d_slabs);
     cudaFree(h->d_out);
+    if (h->cp_stream) {  // copies still in flight write the staging buffers freed below
+        cudaStreamSynchronize(h->cp_stream);
+        cudaStreamDestroy(h->cp_stream);
+    }
     cudaFree(h->d_in_sigma);
     cudaFree(h->d_in_q);
     cudaFree(h->d_in_inflow);
     cudaFree(h->d_in_ready);
-    if (h->cp_stream) {
-        cudaStreamSynchronize(h->cp_stream);
-        cudaStreamDestroy(h->cp_stream);
-    }
     for (auto& e : h->cp_ev)
         if (e) cudaEventDestroy(e);
     delete h;
