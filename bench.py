@@ -443,7 +443,9 @@ def main():
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": job_unknowns / (float(te[0]) * 1e-3), "unit": "unknowns/s",
-               "ms_per_step": float(te[0]), "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": 8 * sw.out_size}
+               "ms_per_step": float(te[0]), "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": 8 * sw.out_size,
+               "copy": ("pinned H2D in 8-row bands overlapping the sweep (per-band ready flags), then D2H"
+                        if prob.dim == 2 else "pinned H2D, sweep, D2H")}
 
     parity = None
     if ws == 1 and not args.no_parity and not opts:
